@@ -1,0 +1,211 @@
+/*
+ * afg.h - C ABI of the B200 (sm_100a) operator kernels behind the AffineForge
+ * graph/operator API.
+ *
+ * The reference executes every operator nest in its CPU interpreter
+ * (af::interpret, /root/reference/proj/include/af/interp.h:97-100, hot loop
+ * proj/src/interp.cpp:440-561). Each entry point below replaces the
+ * interpretation of one operator (or one fused operator chain) of a lowered
+ * graph (proj/src/frontend.cpp:975 lowerGraphToAffine):
+ *
+ *   afg_gemm              <- lowerMatmul            frontend.cpp:679-733
+ *                            + broadcast_in_dim/add/max epilogue nests
+ *                              (frontend.cpp:447-500), fused before the store
+ *   afg_gemm_batched      <- batch_matmul lowering  frontend.cpp:679-733
+ *   afg_conv2d_nhwc       <- lowerConv              frontend.cpp:752-970 as the
+ *                            implicit GEMM of SPEC.md:388-452 (conv_gemm.cpp
+ *                            is a stub in the reference)
+ *   afg_conv2d_nchw       <- lowerConv, direct (general stride/dilation/
+ *                            padding/transposed, frontend.cpp:764-904)
+ *   afg_attention_fwd     <- transpose->batch_matmul->add->softmax->batch_matmul
+ *                            (test_frontend.cpp:275-305; SPEC.md:454-529,
+ *                            attention.cpp is a stub in the reference)
+ *   afg_softmax_lastdim   <- lowerSoftmax           frontend.cpp:564-625
+ *   afg_layernorm_residual<- (no reference op; additive extension)
+ *   afg_elementwise       <- lowerElementwiseBinary frontend.cpp:447-459, exp
+ *   afg_reduce_lastdim    <- lowerReduceShaped      frontend.cpp:628-675
+ *
+ * Conventions
+ *  - All tensor pointers are caller-owned DEVICE pointers, dense row-major
+ *    unless a leading dimension is given. No entry point allocates device
+ *    memory, except the tensor-map cache which is host-side only.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Every call is
+ *    stream-ordered and asynchronous; errors in argument validation are
+ *    reported synchronously, kernel faults surface at the next sync.
+ *  - No C++ exception crosses this boundary. Failures return a status and set
+ *    a thread-local message readable with afg_last_error() (the reference
+ *    reports GraphError / InterpError, frontend.h:26-28, interp.h:29-31).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns AFG_ERR_CUDA.
+ */
+#ifndef AFG_H
+#define AFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AFG_API __attribute__((visibility("default")))
+#else
+#define AFG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum afg_status {
+  AFG_OK = 0,
+  AFG_ERR_INVALID_ARG = 1, /* shape / pointer / alignment contract violated */
+  AFG_ERR_UNSUPPORTED = 2, /* valid request this build has no kernel for      */
+  AFG_ERR_CUDA = 3,        /* CUDA runtime / driver error, or no sm_100 device */
+  AFG_ERR_NCCL = 4,
+  AFG_ERR_INTERNAL = 5
+} afg_status;
+
+/* Element types. F32/F16 mirror af::ElementType (ir.h:29); BF16 is the
+ * additive extension the BASELINE configs need (the reference carries bf16
+ * values in f32 tensors). */
+typedef enum afg_dtype { AFG_F32 = 0, AFG_F16 = 1, AFG_BF16 = 2 } afg_dtype;
+
+/* y = act(acc + bias[n]); NONE ignores bias. */
+typedef enum afg_epilogue {
+  AFG_EPI_NONE = 0,
+  AFG_EPI_BIAS = 1,
+  AFG_EPI_BIAS_RELU = 2,      /* max(acc + bias, 0): the graph's max(x, zeros) */
+  AFG_EPI_BIAS_GELU_TANH = 3, /* x * sigmoid(2u), u = sqrt(2/pi)(x + .044715x^3) */
+  AFG_EPI_BIAS_GELU_ERF = 4   /* 0.5 x (1 + erf(x / sqrt 2)) (BERT)              */
+} afg_epilogue;
+
+/* Storage of the B operand of a GEMM. The reference matmul is A[M,K] x B[K,N]
+ * (frontend.cpp:679-733), i.e. AFG_B_KN. AFG_B_NK stores B transposed
+ * ([N,K] row-major, e.g. packed conv filters / linear weights). */
+typedef enum afg_layout { AFG_B_KN = 0, AFG_B_NK = 1 } afg_layout;
+
+typedef enum afg_binop {
+  AFG_OP_ADD = 0,
+  AFG_OP_SUB = 1,
+  AFG_OP_MUL = 2,
+  AFG_OP_MAX = 3,
+  AFG_OP_EXP = 4 /* unary: b ignored */
+} afg_binop;
+
+typedef enum afg_reduce_kind { AFG_REDUCE_SUM = 0, AFG_REDUCE_MAX = 1 } afg_reduce_kind;
+
+/* ------------------------------------------------------------ runtime --- */
+
+AFG_API const char* afg_last_error(void);
+AFG_API const char* afg_version(void);
+/* Number of visible devices with compute capability 10.x (0 if none). */
+AFG_API int afg_device_count(void);
+/* Number of afg kernel launches issued by this process so far (all entry
+ * points, all devices); bench.py uses it to report gpu_launches. */
+AFG_API uint64_t afg_launch_count(void);
+
+/* ------------------------------------------------------------ GEMM (K1) --- */
+
+/* C[M,N] = epi(A[M,K] . B + bias) (+ residual[M,N]).
+ *  - ab_dtype BF16/F16: tcgen05 tensor-core kernel, fp32 accumulation in TMEM.
+ *    Requires lda, ldb multiples of 8 elements and 16-byte aligned A, B;
+ *    other shapes run the SIMT kernel.
+ *  - ab_dtype F32: fp32 SIMT kernel (FFMA, fp32 accumulation).
+ *  - c_dtype may differ from ab_dtype; bias is fp32 [N] (may be NULL only if
+ *    epi == AFG_EPI_NONE); residual has c_dtype and leading dimension ldc.
+ * Leading dimensions are in elements. */
+AFG_API afg_status afg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb,
+                    const float* bias, const void* residual, void* C, int64_t ldc,
+                    int64_t M, int64_t N, int64_t K, afg_dtype ab_dtype, afg_dtype c_dtype,
+                    afg_layout b_layout, afg_epilogue epi, void* stream);
+
+/* Strided-batched C_b = A_b . B_b (batch_matmul, frontend.cpp:679-733 with
+ * batch dims): all operands dense row-major [batch, rows, cols], B is
+ * [batch, K, N]. No epilogue. */
+AFG_API afg_status afg_gemm_batched(const void* A, const void* B, void* C, int64_t batch,
+                            int64_t M, int64_t N, int64_t K, afg_dtype ab_dtype,
+                            afg_dtype c_dtype, void* stream);
+
+/* ------------------------------------------------------------ conv (K2) --- */
+
+/* Implicit-GEMM convolution, NHWC activations:
+ *   x [B,H,W,C], w [OC,KH,KW,C] (K-major filter), y [B,OH,OW,OC]
+ *   y = epi(conv(x, w) + bias)
+ * GEMM view: M = B*OH*OW, N = OC, K = KH*KW*C. Explicit
+ * asymmetric-capable padding: input row iy = oy*stride_h + ky*dil_h - pad_top.
+ * dtype BF16/F16 (tensor cores; C % 64 == 0 for the TMA path) or F32. */
+AFG_API afg_status afg_conv2d_nhwc(const void* x, const void* w, const float* bias, void* y,
+                           int64_t B, int64_t H, int64_t W, int64_t C, int64_t OC,
+                           int64_t KH, int64_t KW, int64_t stride_h, int64_t stride_w,
+                           int64_t pad_top, int64_t pad_left, int64_t dil_h,
+                           int64_t dil_w, int64_t OH, int64_t OW, afg_dtype dtype,
+                           afg_epilogue epi, void* stream);
+
+/* Direct convolution in the reference's own NCHW/OIHW layout (and IOHW for
+ * transposed), exactly the semantics of frontend.cpp:752-970 / the oracle
+ * convReference (oracles.cpp:78-120), fp32 accumulate. pad_* are the begin
+ * pads of convGeometry (frontend.cpp:115-149). */
+AFG_API afg_status afg_conv2d_nchw(const void* x, const void* w, void* y, int64_t B, int64_t C,
+                           int64_t H, int64_t W, int64_t OC, int64_t KH, int64_t KW,
+                           int64_t stride_h, int64_t stride_w, int64_t dil_h,
+                           int64_t dil_w, int64_t pad_top, int64_t pad_left,
+                           int transposed, int64_t OH, int64_t OW, afg_dtype x_dtype,
+                           afg_dtype y_dtype, void* stream);
+
+/* OIHW -> OHWI filter repack for afg_conv2d_nhwc. */
+AFG_API afg_status afg_conv_pack_filter(const void* w_oihw, void* w_ohwi, int64_t OC, int64_t C,
+                                int64_t KH, int64_t KW, afg_dtype dtype, void* stream);
+
+/* ------------------------------------------------------- attention (K3) --- */
+
+/* o = softmax(scale * q k^T + bias [+ causal mask]) v, per (b, h):
+ *   q [B,H,Nq,D], k/v [B,H,Nk,D], o [B,H,Nq,D], bias [B,H,Nq,Nk] fp32 or NULL.
+ * causal: key j is masked for j > i (the -inf additive bias of SURVEY.md §8a8).
+ * The reference has no scale (scale = 1 reproduces it). dtype F16/BF16 runs
+ * the tcgen05 flash kernel (D in {64,128}); F32 runs the SIMT kernel.
+ * Output dtype o_dtype (F32 keeps the reference's unrounded output). */
+AFG_API afg_status afg_attention_fwd(const void* q, const void* k, const void* v,
+                             const float* bias, void* o, int64_t B, int64_t H,
+                             int64_t Nq, int64_t Nk, int64_t D, float scale, int causal,
+                             afg_dtype dtype, afg_dtype o_dtype, void* stream);
+
+/* ------------------------------------------------- memory-bound chains --- */
+
+/* Row softmax over the last axis (frontend.cpp:564-625 / oracles.cpp:175-190). */
+AFG_API afg_status afg_softmax_lastdim(const void* x, void* y, int64_t rows, int64_t cols,
+                               afg_dtype x_dtype, afg_dtype y_dtype, void* stream);
+
+/* y = layernorm(x + residual) * gamma + beta over the last axis, biased
+ * variance, fp32 statistics. residual may be NULL. Also writes the sum
+ * x + residual to `sum_out` when non-NULL. */
+AFG_API afg_status afg_layernorm_residual(const void* x, const void* residual, const float* gamma,
+                                  const float* beta, void* y, void* sum_out, int64_t rows,
+                                  int64_t cols, float eps, afg_dtype dtype, void* stream);
+
+/* out = op(a, b) elementwise over n elements; b may be broadcast along the
+ * last axis when b_period > 0 (b[i % b_period]). */
+AFG_API afg_status afg_elementwise(const void* a, const void* b, void* out, int64_t n,
+                           int64_t b_period, afg_binop op, afg_dtype a_dtype,
+                           afg_dtype b_dtype, afg_dtype out_dtype, void* stream);
+
+/* out[r] = reduce(x[r, 0:cols]) */
+AFG_API afg_status afg_reduce_lastdim(const void* x, void* out, int64_t rows, int64_t cols,
+                              afg_reduce_kind kind, afg_dtype x_dtype, afg_dtype out_dtype,
+                              void* stream);
+
+/* Dtype conversion (RNE), used by the graph executor's host staging. */
+AFG_API afg_status afg_convert(const void* x, void* y, int64_t n, afg_dtype x_dtype,
+                       afg_dtype y_dtype, void* stream);
+
+/* General permutation of a dense tensor (rank <= 6): y = transpose(x, perm). */
+AFG_API afg_status afg_transpose(const void* x, void* y, int rank, const int64_t* shape,
+                         const int64_t* perm, afg_dtype dtype, void* stream);
+
+/* Deterministic synthetic inputs on device: x[i] = lo + u_i (hi - lo),
+ * u_i from splitmix64(seed, i), rounded (RNE) to `dtype`. */
+AFG_API afg_status afg_fill_uniform(void* x, int64_t n, uint64_t seed, float lo, float hi,
+                            afg_dtype dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AFG_H */

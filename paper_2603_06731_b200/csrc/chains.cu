@@ -1,0 +1,560 @@
+// chains.cu - K4/K5/K6: the memory-bound fused chains.
+//
+// The reference lowers softmax to four nests with global intermediates
+// (.rowmax / .exp / .rowsum, frontend.cpp:564-625) and its fusion pass leaves
+// them as four nests (probe 3). Here each chain is ONE pass
+// over HBM: 128-bit vectorised coalesced loads (the reference's
+// maxVectorWidthElems = 8 x 16-bit, ir.h:213), the row kept in registers,
+// warp-shuffle reductions, one 128-bit store per chunk.
+//
+//   softmax_lastdim     : y = exp(x - max) / sum exp(x - max)   (oracles.cpp:175-190)
+//   layernorm_residual  : y = (s - mean) * rsqrt(var + eps) * gamma + beta,
+//                         s = x + residual, biased variance, fp32 statistics
+//   elementwise / reduce / convert / transpose / fill: graph-executor tails
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "afg_internal.h"
+#include "epilogue.cuh"
+
+namespace afg {
+namespace {
+
+// ------------------------------------------------------------ utilities --
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T>
+struct Vec {  // one 16-byte chunk
+  static constexpr int N = 16 / sizeof(T);
+  union {
+    uint4 u;
+    T e[N];
+  };
+};
+
+__device__ __forceinline__ float ld_any(const void* p, int64_t i, int dt) {
+  switch (dt) {
+    case AFG_F32: return reinterpret_cast<const float*>(p)[i];
+    case AFG_F16: return __half2float(reinterpret_cast<const __half*>(p)[i]);
+    default: return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+  }
+}
+__device__ __forceinline__ void st_any(void* p, int64_t i, int dt, float v) {
+  switch (dt) {
+    case AFG_F32: reinterpret_cast<float*>(p)[i] = v; break;
+    case AFG_F16: reinterpret_cast<__half*>(p)[i] = __float2half_rn(v); break;
+    default: reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v); break;
+  }
+}
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// -------------------------------------------------------------- softmax --
+
+// One warp per row; each lane holds CH 16-byte chunks (chunk c = lane + 32 i).
+template <typename TI, typename TO, int CH>
+__global__ void __launch_bounds__(256) softmax_warp_kernel(const TI* __restrict__ x,
+                                                           TO* __restrict__ y, int64_t rows,
+                                                           int cols) {
+  constexpr int E = Vec<TI>::N;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const int nchunks = cols / E;
+  const TI* xr = x + row * cols;
+  float v[CH][E];
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunks) {
+      Vec<TI> t;
+      t.u = ld_stream(xr + c * E);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        v[i][e] = OutCvt<TI>::from(t.e[e]);
+        m = fmaxf(m, v[i][e]);
+      }
+    }
+  }
+  m = warp_max(m);
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunks) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        v[i][e] = __expf(v[i][e] - m);
+        s += v[i][e];
+      }
+    }
+  }
+  s = warp_sum(s);
+  const float inv = 1.0f / s;
+  TO* yr = y + row * cols;
+  constexpr int EO = Vec<TO>::N;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunks) {
+      if constexpr (EO == E) {
+        Vec<TO> o;
+#pragma unroll
+        for (int e = 0; e < E; ++e) o.e[e] = OutCvt<TO>::to(v[i][e] * inv);
+        st_stream(yr + c * E, o.u);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) yr[c * E + e] = OutCvt<TO>::to(v[i][e] * inv);
+      }
+    }
+  }
+}
+
+// General fallback: one block per row, three sweeps (max, sum, write).
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) softmax_block_kernel(const TI* __restrict__ x,
+                                                            TO* __restrict__ y, int cols) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const TI* xr = x + row * cols;
+  TO* yr = y + row * cols;
+  float m = -INFINITY;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) m = fmaxf(m, OutCvt<TI>::from(xr[c]));
+  m = warp_max(m);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
+    t = warp_max(t);
+    if (threadIdx.x == 0) red[31] = t;
+  }
+  __syncthreads();
+  m = red[31];
+  __syncthreads();
+  float s = 0.0f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) s += __expf(OutCvt<TI>::from(xr[c]) - m);
+  s = warp_sum(s);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[31] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / red[31];
+  for (int c = threadIdx.x; c < cols; c += blockDim.x)
+    yr[c] = OutCvt<TO>::to(__expf(OutCvt<TI>::from(xr[c]) - m) * inv);
+}
+
+template <typename TI, typename TO>
+cudaError_t softmax_launch(const void* x, void* y, int64_t rows, int64_t cols, cudaStream_t s) {
+  constexpr int E = Vec<TI>::N;
+  const bool vec_ok = (cols % E == 0) && (cols % Vec<TO>::N == 0) &&
+                      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  const int64_t nchunks = cols / E;
+  const TI* xi = reinterpret_cast<const TI*>(x);
+  TO* yo = reinterpret_cast<TO*>(y);
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  if (vec_ok && nchunks <= 32 * 16 && rows / 8 < (1ll << 31)) {
+    if (nchunks <= 32)
+      softmax_warp_kernel<TI, TO, 1><<<grid, 256, 0, s>>>(xi, yo, rows, (int)cols);
+    else if (nchunks <= 64)
+      softmax_warp_kernel<TI, TO, 2><<<grid, 256, 0, s>>>(xi, yo, rows, (int)cols);
+    else if (nchunks <= 128)
+      softmax_warp_kernel<TI, TO, 4><<<grid, 256, 0, s>>>(xi, yo, rows, (int)cols);
+    else if (nchunks <= 256)
+      softmax_warp_kernel<TI, TO, 8><<<grid, 256, 0, s>>>(xi, yo, rows, (int)cols);
+    else
+      softmax_warp_kernel<TI, TO, 16><<<grid, 256, 0, s>>>(xi, yo, rows, (int)cols);
+  } else {
+    if (rows >= (1ll << 31)) return cudaErrorInvalidValue;
+    softmax_block_kernel<TI, TO><<<static_cast<unsigned>(rows), 256, 0, s>>>(xi, yo, (int)cols);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ layernorm --
+
+template <typename T, int CH>
+__global__ void __launch_bounds__(256) layernorm_warp_kernel(
+    const T* __restrict__ x, const T* __restrict__ res, const float* __restrict__ gamma,
+    const float* __restrict__ beta, T* __restrict__ y, T* __restrict__ sum_out, int64_t rows,
+    int cols, float eps) {
+  constexpr int E = Vec<T>::N;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const int nchunks = cols / E;
+  float v[CH][E];
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunks) {
+      Vec<T> a;
+      a.u = ld_stream(x + row * cols + c * E);
+      if (res) {
+        Vec<T> b;
+        b.u = ld_stream(res + row * cols + c * E);
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[i][e] = OutCvt<T>::from(a.e[e]) + OutCvt<T>::from(b.e[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[i][e] = OutCvt<T>::from(a.e[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) s += v[i][e];
+    }
+  }
+  const float mean = warp_sum(s) / cols;
+  float q = 0.0f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunks) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float d = v[i][e] - mean;
+        q = fmaf(d, d, q);
+      }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / cols + eps);
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunks) {
+      Vec<T> o, so;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int col = c * E + e;
+        o.e[e] = OutCvt<T>::to((v[i][e] - mean) * rstd * __ldg(gamma + col) + __ldg(beta + col));
+        so.e[e] = OutCvt<T>::to(v[i][e]);
+      }
+      st_stream(y + row * cols + c * E, o.u);
+      if (sum_out) st_stream(sum_out + row * cols + c * E, so.u);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_block_kernel(
+    const T* __restrict__ x, const T* __restrict__ res, const float* __restrict__ gamma,
+    const float* __restrict__ beta, T* __restrict__ y, T* __restrict__ sum_out, int cols,
+    float eps) {
+  __shared__ float red[33];
+  const int64_t row = blockIdx.x;
+  auto val = [&](int c) {
+    float v = OutCvt<T>::from(x[row * cols + c]);
+    if (res) v += OutCvt<T>::from(res[row * cols + c]);
+    return v;
+  };
+  auto block_sum = [&](float v) {
+    v = warp_sum(v);
+    __syncthreads();
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+  };
+  float s = 0.0f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) s += val(c);
+  const float mean = block_sum(s) / cols;
+  float q = 0.0f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float d = val(c) - mean;
+    q = fmaf(d, d, q);
+  }
+  const float rstd = rsqrtf(block_sum(q) / cols + eps);
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = val(c);
+    y[row * cols + c] = OutCvt<T>::to((v - mean) * rstd * gamma[c] + beta[c]);
+    if (sum_out) sum_out[row * cols + c] = OutCvt<T>::to(v);
+  }
+}
+
+template <typename T>
+cudaError_t layernorm_launch(const void* x, const void* r, const float* g, const float* b,
+                             void* y, void* so, int64_t rows, int64_t cols, float eps,
+                             cudaStream_t s) {
+  constexpr int E = Vec<T>::N;
+  const uintptr_t addr_or = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) |
+                            reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(so);
+  const bool vec_ok = cols % E == 0 && (addr_or & 15) == 0;
+  const int64_t nchunks = cols / E;
+  const T* xi = reinterpret_cast<const T*>(x);
+  const T* ri = reinterpret_cast<const T*>(r);
+  T* yo = reinterpret_cast<T*>(y);
+  T* soo = reinterpret_cast<T*>(so);
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  if (vec_ok && nchunks <= 32 * 16) {
+#define AFG_LN(CH) \
+  layernorm_warp_kernel<T, CH><<<grid, 256, 0, s>>>(xi, ri, g, b, yo, soo, rows, (int)cols, eps)
+    if (nchunks <= 32) AFG_LN(1);
+    else if (nchunks <= 64) AFG_LN(2);
+    else if (nchunks <= 96) AFG_LN(3);
+    else if (nchunks <= 128) AFG_LN(4);
+    else if (nchunks <= 256) AFG_LN(8);
+    else AFG_LN(16);
+#undef AFG_LN
+  } else {
+    layernorm_block_kernel<T><<<static_cast<unsigned>(rows), 256, 0, s>>>(xi, ri, g, b, yo, soo,
+                                                                         (int)cols, eps);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- elementwise --
+
+__global__ void elementwise_kernel(const void* __restrict__ a, const void* __restrict__ b,
+                                   void* __restrict__ out, int64_t n, int64_t b_period, int op,
+                                   int adt, int bdt, int odt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float x = ld_any(a, i, adt);
+    float r;
+    if (op == AFG_OP_EXP) {
+      r = expf(x);
+    } else {
+      const float y = ld_any(b, b_period > 0 ? i % b_period : i, bdt);
+      switch (op) {
+        case AFG_OP_ADD: r = x + y; break;
+        case AFG_OP_SUB: r = x - y; break;
+        case AFG_OP_MUL: r = x * y; break;
+        default: r = fmaxf(x, y); break;
+      }
+    }
+    st_any(out, i, odt, r);
+  }
+}
+
+__global__ void reduce_kernel(const void* __restrict__ x, void* __restrict__ out, int64_t rows,
+                              int64_t cols, int kind, int xdt, int odt) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  float acc = kind == AFG_REDUCE_MAX ? -INFINITY : 0.0f;
+  for (int64_t c = lane; c < cols; c += 32) {
+    const float v = ld_any(x, row * cols + c, xdt);
+    acc = kind == AFG_REDUCE_MAX ? fmaxf(acc, v) : acc + v;
+  }
+  acc = kind == AFG_REDUCE_MAX ? warp_max(acc) : warp_sum(acc);
+  if (lane == 0) st_any(out, row, odt, acc);
+}
+
+__global__ void convert_kernel(const void* __restrict__ x, void* __restrict__ y, int64_t n,
+                               int xdt, int ydt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    st_any(y, i, ydt, ld_any(x, i, xdt));
+}
+
+struct TransposeArgs {
+  int rank;
+  int64_t out_shape[6];
+  int64_t in_stride_for_out[6];  // input stride of the input dim mapped to out dim d
+};
+
+__global__ void transpose_kernel(const void* __restrict__ x, void* __restrict__ y, int64_t n,
+                                 TransposeArgs t, int esize) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t rem = i, src = 0;
+    for (int d = t.rank - 1; d >= 0; --d) {
+      const int64_t idx = rem % t.out_shape[d];
+      rem /= t.out_shape[d];
+      src += idx * t.in_stride_for_out[d];
+    }
+    if (esize == 4)
+      reinterpret_cast<float*>(y)[i] = reinterpret_cast<const float*>(x)[src];
+    else
+      reinterpret_cast<uint16_t*>(y)[i] = reinterpret_cast<const uint16_t*>(x)[src];
+  }
+}
+
+// splitmix64 as in makeRandomTensor (interp.cpp:817-844): the i-th draw of a
+// stream seeded with s0 is mix(s0 + (i + 1) * golden), so the whole tensor is
+// generated in parallel and bit-identical to the reference generator.
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t s0, uint64_t i) {
+  uint64_t z = s0 + (i + 1) * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_uniform_kernel(void* __restrict__ x, int64_t n, uint64_t seed, double lo,
+                                    double hi, int dt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t bits = splitmix_at(seed, static_cast<uint64_t>(i));
+    const double u = static_cast<double>(bits >> 11) * (1.0 / 9007199254740992.0);
+    const double v = lo + u * (hi - lo);
+    switch (dt) {
+      case AFG_F32: reinterpret_cast<float*>(x)[i] = static_cast<float>(v); break;
+      case AFG_F16:
+        reinterpret_cast<__half*>(x)[i] = __float2half_rn(static_cast<float>(v));
+        break;
+      default:
+        reinterpret_cast<__nv_bfloat16*>(x)[i] = __float2bfloat16_rn(static_cast<float>(v));
+        break;
+    }
+  }
+}
+
+unsigned grid_for(int64_t n, int per_block = 256) {
+  int64_t g = (n + per_block - 1) / per_block;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+bool valid_dt(int t) { return t == AFG_F32 || t == AFG_F16 || t == AFG_BF16; }
+
+}  // namespace
+}  // namespace afg
+
+using namespace afg;
+
+extern "C" {
+
+afg_status afg_softmax_lastdim(const void* x, void* y, int64_t rows, int64_t cols,
+                               afg_dtype xd, afg_dtype yd, void* stream) {
+  if (!x || !y || rows <= 0 || cols <= 0 || !valid_dt(xd) || !valid_dt(yd))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_softmax_lastdim: bad arguments");
+  if (cols >= (1ll << 31)) return set_error(AFG_ERR_UNSUPPORTED, "softmax: cols too large");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+#define AFG_SM(TI, TO) e = softmax_launch<TI, TO>(x, y, rows, cols, s)
+  if (xd == AFG_F32 && yd == AFG_F32) AFG_SM(float, float);
+  else if (xd == AFG_F16 && yd == AFG_F16) AFG_SM(__half, __half);
+  else if (xd == AFG_BF16 && yd == AFG_BF16) AFG_SM(__nv_bfloat16, __nv_bfloat16);
+  else if (xd == AFG_F16 && yd == AFG_F32) AFG_SM(__half, float);
+  else if (xd == AFG_BF16 && yd == AFG_F32) AFG_SM(__nv_bfloat16, float);
+  else if (xd == AFG_F32 && yd == AFG_F16) AFG_SM(float, __half);
+  else AFG_SM(float, __nv_bfloat16);
+#undef AFG_SM
+  return cuda_status(e, "softmax launch");
+}
+
+afg_status afg_layernorm_residual(const void* x, const void* residual, const float* gamma,
+                                  const float* beta, void* y, void* sum_out, int64_t rows,
+                                  int64_t cols, float eps, afg_dtype dtype, void* stream) {
+  if (!x || !y || !gamma || !beta || rows <= 0 || cols <= 0 || !valid_dt(dtype))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_layernorm_residual: bad arguments");
+  if (cols >= (1ll << 31) || rows >= (1ll << 31))
+    return set_error(AFG_ERR_UNSUPPORTED, "layernorm: extent too large");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (dtype == AFG_F32)
+    e = layernorm_launch<float>(x, residual, gamma, beta, y, sum_out, rows, cols, eps, s);
+  else if (dtype == AFG_F16)
+    e = layernorm_launch<__half>(x, residual, gamma, beta, y, sum_out, rows, cols, eps, s);
+  else
+    e = layernorm_launch<__nv_bfloat16>(x, residual, gamma, beta, y, sum_out, rows, cols, eps,
+                                        s);
+  return cuda_status(e, "layernorm launch");
+}
+
+afg_status afg_elementwise(const void* a, const void* b, void* out, int64_t n, int64_t b_period,
+                           afg_binop op, afg_dtype ad, afg_dtype bd, afg_dtype od,
+                           void* stream) {
+  if (!a || !out || n <= 0 || (op != AFG_OP_EXP && !b) || op < AFG_OP_ADD || op > AFG_OP_EXP ||
+      !valid_dt(ad) || !valid_dt(od) || (op != AFG_OP_EXP && !valid_dt(bd)))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_elementwise: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  elementwise_kernel<<<grid_for(n), 256, 0, s>>>(a, b, out, n, b_period, op, ad, bd, od);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "elementwise launch");
+}
+
+afg_status afg_reduce_lastdim(const void* x, void* out, int64_t rows, int64_t cols,
+                              afg_reduce_kind kind, afg_dtype xd, afg_dtype od, void* stream) {
+  if (!x || !out || rows <= 0 || cols <= 0 || !valid_dt(xd) || !valid_dt(od))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_reduce_lastdim: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  reduce_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, out, rows, cols, kind,
+                                                                     xd, od);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "reduce launch");
+}
+
+afg_status afg_convert(const void* x, void* y, int64_t n, afg_dtype xd, afg_dtype yd,
+                       void* stream) {
+  if (!x || !y || n <= 0 || !valid_dt(xd) || !valid_dt(yd))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_convert: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  convert_kernel<<<grid_for(n), 256, 0, s>>>(x, y, n, xd, yd);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "convert launch");
+}
+
+afg_status afg_transpose(const void* x, void* y, int rank, const int64_t* shape,
+                         const int64_t* perm, afg_dtype dtype, void* stream) {
+  if (!x || !y || !shape || !perm || rank <= 0 || rank > 6 || !valid_dt(dtype))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_transpose: bad arguments");
+  TransposeArgs t;
+  t.rank = rank;
+  int64_t in_stride[6];
+  int64_t st = 1, n = 1;
+  for (int d = rank - 1; d >= 0; --d) {
+    in_stride[d] = st;
+    st *= shape[d];
+  }
+  bool seen[6] = {false, false, false, false, false, false};
+  for (int d = 0; d < rank; ++d) {
+    if (perm[d] < 0 || perm[d] >= rank || seen[perm[d]])
+      return set_error(AFG_ERR_INVALID_ARG, "afg_transpose: bad perm");
+    seen[perm[d]] = true;
+    t.out_shape[d] = shape[perm[d]];
+    t.in_stride_for_out[d] = in_stride[perm[d]];
+    n *= shape[d];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  transpose_kernel<<<grid_for(n), 256, 0, s>>>(x, y, n, t, dtype_bytes(dtype));
+  count_launch();
+  return cuda_status(cudaGetLastError(), "transpose launch");
+}
+
+afg_status afg_fill_uniform(void* x, int64_t n, uint64_t seed, float lo, float hi,
+                            afg_dtype dtype, void* stream) {
+  if (!x || n <= 0 || !valid_dt(dtype))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_fill_uniform: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  fill_uniform_kernel<<<grid_for(n), 256, 0, s>>>(x, n, seed, lo, hi, dtype);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "fill launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// epilogue.cuh - the fused elementwise tail of the contraction kernels.
+//
+// Realises the graph chain the reference lowers as separate nests after a
+// matmul / conv2d (frontend.cpp:447-500 broadcast_in_dim+add, max(x, zeros)):
+//   y = act(acc + bias[n]) (+ residual[m, n])
+// applied to the fp32 accumulator before the single store, which is the
+// "fusion into copy-out" the paper describes and that the
+// reference's own fusion pass never performs (nest 3).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "../../include/afg.h"
+
+namespace afg {
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  // x * sigmoid(2u), u = sqrt(2/pi) (x + 0.044715 x^3): the composite the
+  // reference graph API expresses with a size-2 softmax.
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  return x / (1.0f + __expf(-2.0f * u));
+}
+
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.7071067811865476f));
+}
+
+template <int EPI>
+__device__ __forceinline__ float apply_act(float v) {
+  if constexpr (EPI == AFG_EPI_BIAS_RELU) return fmaxf(v, 0.0f);
+  if constexpr (EPI == AFG_EPI_BIAS_GELU_TANH) return gelu_tanh(v);
+  if constexpr (EPI == AFG_EPI_BIAS_GELU_ERF) return gelu_erf(v);
+  return v;
+}
+
+// Runtime dispatch over the epilogue kind for kernels that do not template it.
+__device__ __forceinline__ float apply_act_rt(int epi, float v) {
+  switch (epi) {
+    case AFG_EPI_BIAS_RELU: return fmaxf(v, 0.0f);
+    case AFG_EPI_BIAS_GELU_TANH: return gelu_tanh(v);
+    case AFG_EPI_BIAS_GELU_ERF: return gelu_erf(v);
+    default: return v;
+  }
+}
+
+template <typename T> struct OutCvt;
+template <> struct OutCvt<float> {
+  static __device__ __forceinline__ float to(float v) { return v; }
+  static __device__ __forceinline__ float from(float v) { return v; }
+};
+template <> struct OutCvt<__nv_bfloat16> {
+  static __device__ __forceinline__ __nv_bfloat16 to(float v) { return __float2bfloat16_rn(v); }
+  static __device__ __forceinline__ float from(__nv_bfloat16 v) { return __bfloat162float(v); }
+};
+template <> struct OutCvt<__half> {
+  static __device__ __forceinline__ __half to(float v) { return __float2half_rn(v); }
+  static __device__ __forceinline__ float from(__half v) { return __half2float(v); }
+};
+
+}  // namespace afg

@@ -1,0 +1,377 @@
+// gemm_tc.cu - K1: bf16/fp16 GEMM on 5th-gen tensor cores with the fused
+// bias / ReLU / GELU (+ residual) epilogue.
+//
+// What the reference describes and this kernel realises natively:
+//   * multi-level tiling + scratchpad promotion (orchestrate, tiling.cpp:
+//     1059-1203; measured structure SURVEY.md §3.2): the 64x64x32 block tile
+//     with double-buffered shared A/B tiles becomes a 128 x BLOCK_N x 64 tile
+//     fed by a STAGES-deep TMA ring (cp.async.bulk.tensor + mbarrier
+//     expect_tx), honouring the interpreter's "no use before await" rule
+//     (interp.cpp:314-318, 657-685) through full/empty barrier phases;
+//   * the shared C tile becomes a TMEM accumulator (tcgen05.mma kind::f16,
+//     fp32), double-buffered so the epilogue of tile i overlaps the MMAs of
+//     tile i+1;
+//   * the 16x16 fragment mapping (mmaHook, tiling.h:96) is a
+//     single-thread-issued 128 x BLOCK_N x 16 UMMA;
+//   * the bias+max epilogue nest (left unfused by the reference) is applied
+//     to the accumulator in registers before the one global store.
+//
+// Warp roles (256 threads, 1 CTA per SM, persistent over output tiles):
+//   warp 0  : TMA producer (one elected lane)
+//   warp 1  : MMA issuer   (one lane)
+//   warp 2  : TMEM allocator / deallocator
+//   warps 4-7: epilogue (thread t owns accumulator row t of the tile)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "afg_internal.h"
+#include "epilogue.cuh"
+#include "sm100.cuh"
+
+namespace afg {
+namespace {
+
+using namespace sm100;
+
+constexpr int BLOCK_M = 128;
+constexpr int BLOCK_K = 64;  // 64 x 16-bit = one 128-byte swizzle row
+constexpr int GROUP_M = 16;  // tile raster: 16 M-blocks share B tiles in L2
+
+struct GemmTcArgs {
+  int M, N, K;
+  int ldc;
+  const float* bias;
+  const void* residual;
+  void* C;
+  int num_m_blocks, num_n_blocks;
+  int epi;
+};
+
+template <int BLOCK_N, int STAGES>
+struct SmemLayout {
+  static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 2;
+  static constexpr int B_BYTES = BLOCK_N * BLOCK_K * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int NUM_BARS = 2 * STAGES + 4;
+  static constexpr int TOTAL = BAR_OFFSET + NUM_BARS * 8 + 16 + 1024;  // +1024 align slack
+};
+
+__device__ __forceinline__ void tile_coords(int t, int nmb, int nnb, int& mb, int& nb) {
+  const int per_group = GROUP_M * nnb;
+  const int group = t / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(nmb - first_m, GROUP_M);
+  const int r = t - group * per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int EPI, typename OutT>
+__device__ __forceinline__ void store_chunk32(const uint32_t (&acc)[32], const GemmTcArgs& a,
+                                              int row, int col0) {
+  if (row >= a.M) return;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]);
+  if constexpr (EPI != AFG_EPI_NONE) {
+    if (col0 + 32 <= a.N) {
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias + col0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b = __ldg(b4 + j);
+        v[4 * j + 0] += b.x;
+        v[4 * j + 1] += b.y;
+        v[4 * j + 2] += b.z;
+        v[4 * j + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < a.N) v[j] += __ldg(a.bias + col0 + j);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = apply_act<EPI>(v[j]);
+  }
+  OutT* crow = reinterpret_cast<OutT*>(a.C) + static_cast<int64_t>(row) * a.ldc + col0;
+  const bool HAS_RES = a.residual != nullptr;
+  const OutT* rrow = HAS_RES ? reinterpret_cast<const OutT*>(a.residual) +
+                                   static_cast<int64_t>(row) * a.ldc + col0
+                             : nullptr;
+  const bool full = (col0 + 32 <= a.N) && ((a.ldc & 7) == 0);
+  if (full) {
+    constexpr int PER16 = 16 / sizeof(OutT);  // elements per 16-byte vector
+#pragma unroll
+    for (int j = 0; j < 32 / PER16; ++j) {
+      OutT tmp[PER16];
+      if (HAS_RES) {
+        *reinterpret_cast<uint4*>(tmp) = *reinterpret_cast<const uint4*>(rrow + j * PER16);
+#pragma unroll
+        for (int e = 0; e < PER16; ++e)
+          tmp[e] = OutCvt<OutT>::to(v[j * PER16 + e] + OutCvt<OutT>::from(tmp[e]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < PER16; ++e) tmp[e] = OutCvt<OutT>::to(v[j * PER16 + e]);
+      }
+      *reinterpret_cast<uint4*>(crow + j * PER16) = *reinterpret_cast<uint4*>(tmp);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (col0 + j < a.N) {
+        float r = v[j];
+        if (HAS_RES) r += OutCvt<OutT>::from(rrow[j]);
+        crow[j] = OutCvt<OutT>::to(r);
+      }
+    }
+  }
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], const GemmTcArgs& a,
+                                                 int row, int col0) {
+  switch (a.epi) {
+    case AFG_EPI_BIAS: store_chunk32<AFG_EPI_BIAS, OutT>(acc, a, row, col0); break;
+    case AFG_EPI_BIAS_RELU: store_chunk32<AFG_EPI_BIAS_RELU, OutT>(acc, a, row, col0); break;
+    case AFG_EPI_BIAS_GELU_TANH:
+      store_chunk32<AFG_EPI_BIAS_GELU_TANH, OutT>(acc, a, row, col0);
+      break;
+    case AFG_EPI_BIAS_GELU_ERF: store_chunk32<AFG_EPI_BIAS_GELU_ERF, OutT>(acc, a, row, col0); break;
+    default: store_chunk32<AFG_EPI_NONE, OutT>(acc, a, row, col0); break;
+  }
+}
+
+template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                   const __grid_constant__ CUtensorMap tmB, const GemmTcArgs args) {
+  using L = SmemLayout<BLOCK_N, STAGES>;
+  static_assert(BLOCK_N % 64 == 0 && BLOCK_N <= 256, "BLOCK_N");
+  constexpr uint32_t TMEM_COLS = 2 * BLOCK_N <= 32    ? 32
+                                 : 2 * BLOCK_N <= 64  ? 64
+                                 : 2 * BLOCK_N <= 128 ? 128
+                                 : 2 * BLOCK_N <= 256 ? 256
+                                                      : 512;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + STAGES;
+  uint64_t* tfull_bar = bars + 2 * STAGES;
+  uint64_t* tempty_bar = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = args.num_m_blocks * args.num_n_blocks;
+  const int num_kb = (args.K + BLOCK_K - 1) / BLOCK_K;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::STAGE_BYTES;
+          uint8_t* sb = sa + L::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], L::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full_bar[stage], kb * BLOCK_K, mb * BLOCK_M);
+          if constexpr (B_MN_MAJOR) {
+#pragma unroll
+            for (int j = 0; j < BLOCK_N / 64; ++j)
+              tma_load_2d(sb + j * (64 * BLOCK_K * 2), &tmB, &full_bar[stage],
+                          nb * BLOCK_N + j * 64, kb * BLOCK_K);
+          } else {
+            tma_load_2d(sb, &tmB, &full_bar[stage], kb * BLOCK_K, nb * BLOCK_N);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      constexpr uint32_t idesc =
+          idesc_f16(BLOCK_M, BLOCK_N, AB_BF16 ? 1u : 0u, 0u, B_MN_MAJOR ? 1u : 0u);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+        const int acc = iter & 1;
+        const uint32_t acc_par = (iter >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_par ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * L::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + L::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BLOCK_K / 16; ++k) {
+            const uint64_t adesc = desc_kmajor_sw128(a_addr + k * 32);
+            const uint64_t bdesc = B_MN_MAJOR
+                                       ? desc_mnmajor_sw128(b_addr + k * 16 * 128, 64 * BLOCK_K * 2)
+                                       : desc_kmajor_sw128(b_addr + k * 32);
+            mma_f16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ----------------------------------------------------------- epilogue --
+    const int ew = warp - 4;  // == warp % 4: TMEM lanes [32 ew, 32 ew + 32)
+    int iter = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      int mb, nb;
+      tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+      const int acc = iter & 1;
+      const uint32_t acc_par = (iter >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_par);
+      tc_fence_after();
+      const int row = mb * BLOCK_M + ew * 32 + lane;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
+#pragma unroll 1
+      for (int c = 0; c < BLOCK_N / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(t_row + c * 32, r);
+        tmem_wait_ld();
+        if (c == BLOCK_N / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty_bar[acc]);
+        }
+        const int col0 = nb * BLOCK_N + c * 32;
+        if (col0 < args.N) store_chunk32_rt<OutT>(r, args, row, col0);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// --------------------------------------------------------------- host side --
+
+template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT>
+cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                           const GemmTcArgs& args, cudaStream_t stream) {
+  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT>;
+  constexpr int smem = SmemLayout<BLOCK_N, STAGES>::TOTAL;
+  static bool configured = false;  // per-instantiation, per-process
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int tiles = args.num_m_blocks * args.num_n_blocks;
+  const int grid = std::min(tiles, num_sms());
+  kern<<<grid, 256, smem, stream>>>(tmA, tmB, args);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int BLOCK_N, int STAGES>
+cudaError_t dispatch_types(afg_dtype ab, afg_dtype c, bool b_mn_major, const CUtensorMap& tmA,
+                           const CUtensorMap& tmB, const GemmTcArgs& args, cudaStream_t s) {
+#define AFG_GEMM_V(MN, BF, OT) launch_variant<BLOCK_N, STAGES, MN, BF, OT>(tmA, tmB, args, s)
+  if (ab == AFG_BF16) {
+    if (c == AFG_BF16) return b_mn_major ? AFG_GEMM_V(true, true, __nv_bfloat16)
+                                         : AFG_GEMM_V(false, true, __nv_bfloat16);
+    if (c == AFG_F32) return b_mn_major ? AFG_GEMM_V(true, true, float)
+                                        : AFG_GEMM_V(false, true, float);
+  } else {
+    if (c == AFG_F16) return b_mn_major ? AFG_GEMM_V(true, false, __half)
+                                        : AFG_GEMM_V(false, false, __half);
+    if (c == AFG_F32) return b_mn_major ? AFG_GEMM_V(true, false, float)
+                                        : AFG_GEMM_V(false, false, float);
+  }
+#undef AFG_GEMM_V
+  return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+// Entry used by afg_gemm (api.cpp) and the conv / BERT paths.
+afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const float* bias,
+                   const void* residual, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                   afg_dtype ab, afg_dtype c, afg_layout b_layout, afg_epilogue epi,
+                   cudaStream_t stream) {
+  const bool b_mn_major = b_layout == AFG_B_KN;
+  // BLOCK_N: 256 when N is large enough to fill it, else 128 / 64.
+  const int block_n = N >= 256 ? 256 : (N > 64 ? 128 : 64);
+  const CUtensorMapDataType tdt =
+      ab == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tmA, tmB;
+  afg_status st = make_tmap_2d(&tmA, A, tdt, 2, K, M, lda, BLOCK_K, BLOCK_M);
+  if (st != AFG_OK) return st;
+  if (b_mn_major)
+    st = make_tmap_2d(&tmB, B, tdt, 2, N, K, ldb, 64, BLOCK_K);
+  else
+    st = make_tmap_2d(&tmB, B, tdt, 2, K, N, ldb, BLOCK_K, block_n);
+  if (st != AFG_OK) return st;
+
+  GemmTcArgs args;
+  args.M = static_cast<int>(M);
+  args.N = static_cast<int>(N);
+  args.K = static_cast<int>(K);
+  args.ldc = static_cast<int>(ldc);
+  args.bias = bias;
+  args.residual = residual;
+  args.C = C;
+  args.num_m_blocks = static_cast<int>((M + BLOCK_M - 1) / BLOCK_M);
+  args.num_n_blocks = static_cast<int>((N + block_n - 1) / block_n);
+  args.epi = static_cast<int>(epi);
+  cudaError_t e;
+  if (block_n == 256)
+    e = dispatch_types<256, 4>(ab, c, b_mn_major, tmA, tmB, args, stream);
+  else if (block_n == 128)
+    e = dispatch_types<128, 6>(ab, c, b_mn_major, tmA, tmB, args, stream);
+  else
+    e = dispatch_types<64, 8>(ab, c, b_mn_major, tmA, tmB, args, stream);
+  if (e == cudaErrorNotSupported)
+    return set_error(AFG_ERR_UNSUPPORTED, "gemm_tc: unsupported (ab, c) dtype pair");
+  return cuda_status(e, "gemm_tc launch");
+}
+
+}  // namespace afg
