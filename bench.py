@@ -1,0 +1,508 @@
+#!/usr/bin/env python3
+"""bench.py - headline benchmark of the afg B200 kernels (BASELINE.json).
+
+Default workload (BASELINE configs[1]): bf16 matmul 16384^3, fp32
+accumulation, fused bias + tanh-GELU epilogue, row-sharded across ranks
+(strong scaling: the 16384^3 problem is fixed, each rank computes M/N rows
+against the full B). One step = one pass of the hot path (one fused GEMM
+launch) over one batch of synthetic input already resident in HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                    [--impl afg|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL for barriers and the
+max-over-ranks reduction of the device time; no data-path collective).
+--impl reference times the reference's own CPU path (the AffineForge
+interpreter, oracle/_ref, or the oracle C port if it is absent) on the
+host cores with every thread, on a bounded sample of the same workload.
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained"), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback"}
+
+
+def traffic_for(workload):
+    try:
+        with open(TRAFFIC_FILE) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------- clocks ---
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    self.samples.append(parts)
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=1)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for p in self.samples:
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------- distributed ---
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard_rows(total, rank, world):
+    """Contiguous row shard [begin, end) of `total` rows for `rank`."""
+    base, rem = divmod(total, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+def shard_seed(s0, first_element):
+    """Stream state whose draw i equals draw first_element + i of stream s0
+    (splitmix64 advances its state by the golden constant per draw)."""
+    return (s0 + first_element * 0x9E3779B97F4A7C15) & (2**64 - 1)
+
+
+# ============================================================ workloads ===
+
+class GemmBF16:
+    """BASELINE configs[1]: bf16 C = gelu_tanh(A B + bias), fp32 accumulate."""
+
+    name = "gemm_bf16_gelu"
+
+    def __init__(self, size):
+        self.n = size
+
+    def config(self, world):
+        return {"workload": f"bf16 matmul {self.n}x{self.n}x{self.n} + bias + tanh-GELU "
+                            f"epilogue (fp32 accumulate), row-sharded",
+                "M": self.n, "N": self.n, "K": self.n, "parallelism": f"rows/{world}",
+                "l2": "operands larger than L2 (no flush needed)",
+                "sweep": "2048-16384 via --size"}
+
+    metric = "TFLOP/s"
+    unit = "TFLOP/s"
+    dtype = "bf16"
+    bound = "tensor"
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        from paper_2603_06731_b200 import ops
+        self.torch = torch
+        self.ops = ops
+        r0, r1 = shard_rows(self.n, rank, world)
+        self.m = r1 - r0
+        import oracle  # generator seed only: the data are made on the device
+        self.A = ops.fill_uniform((self.m, self.n), shard_seed(oracle.stream_seed("%a", 1),
+                                                               r0 * self.n), -1, 1, torch.bfloat16)
+        self.B = ops.fill_uniform((self.n, self.n), oracle.stream_seed("%b", 1), -1, 1,
+                                  torch.bfloat16)
+        self.bias = ops.fill_uniform((self.n,), oracle.stream_seed("%bias", 1), -1, 1,
+                                     torch.float32)
+        self.C = torch.empty((self.m, self.n), dtype=torch.bfloat16, device=dev)
+        self.flops_rank = 2.0 * self.m * self.n * self.n
+        self.flops_total = 2.0 * self.n ** 3
+        self.alg_bytes_rank = 2.0 * (self.m * self.n + self.n * self.n + self.m * self.n) + 4 * self.n
+
+    def step(self):
+        from paper_2603_06731_b200 import Epilogue
+        self.ops.gemm(self.A, self.B, bias=self.bias, epilogue=Epilogue.BIAS_GELU_TANH, out=self.C)
+
+    def launches_per_step(self):
+        return 1
+
+    # e2e: pinned host bf16 buffers -> H2D -> afg_gemm (C ABI) -> D2H
+    def e2e_setup(self):
+        t = self.torch
+        self.hA = self.A.cpu().pin_memory()
+        self.hB = self.B.cpu().pin_memory()
+        self.hbias = self.bias.cpu().pin_memory()
+        self.hC = t.empty((self.m, self.n), dtype=t.bfloat16).pin_memory()
+        self.dA = t.empty_like(self.A)
+        self.dB = t.empty_like(self.B)
+        self.dbias = t.empty_like(self.bias)
+        self.h2d = self.hA.numel() * 2 + self.hB.numel() * 2 + self.hbias.numel() * 4
+        self.d2h = self.hC.numel() * 2
+
+    def e2e_step(self):
+        from paper_2603_06731_b200 import Epilogue
+        self.dA.copy_(self.hA, non_blocking=True)
+        self.dB.copy_(self.hB, non_blocking=True)
+        self.dbias.copy_(self.hbias, non_blocking=True)
+        self.ops.gemm(self.dA, self.dB, bias=self.dbias, epilogue=Epilogue.BIAS_GELU_TANH,
+                      out=self.C)
+        self.hC.copy_(self.C, non_blocking=True)
+
+    # bounded CPU sample of the same workload through the reference path
+    def reference_sample(self, threads):
+        return ReferenceGemmSample(self.n, threads)
+
+
+class GemmFP32:
+    """BASELINE configs[0]: fp32 1024^3 + bias + ReLU (replicas only)."""
+
+    name = "gemm_fp32_relu"
+    metric = "TFLOP/s"
+    unit = "TFLOP/s"
+    dtype = "f32"
+    bound = "fp32-simt"
+
+    def __init__(self, size=1024):
+        self.n = size
+
+    def config(self, world):
+        return {"workload": f"fp32 matmul {self.n}^3 + bias + ReLU (the reference's own "
+                            f"operator test), bit-exact vs af::interpret",
+                "parallelism": f"replicas/{world}", "l2": "L2 flushed between steps"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        import oracle
+        from paper_2603_06731_b200 import ops
+        self.torch, self.ops = torch, ops
+        n = self.n
+        self.A = ops.fill_uniform((n, n), oracle.stream_seed("%a", 1), -1, 1, torch.float32)
+        self.B = ops.fill_uniform((n, n), oracle.stream_seed("%b", 2), -1, 1, torch.float32)
+        self.bias = ops.fill_uniform((n,), oracle.stream_seed("%bias", 3), -1, 1, torch.float32)
+        self.C = torch.empty((n, n), dtype=torch.float32, device=dev)
+        self.flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+        self.flops_rank = self.flops_total = 2.0 * n ** 3
+        self.alg_bytes_rank = 4.0 * 3 * n * n
+
+    def step(self):
+        from paper_2603_06731_b200 import Epilogue
+        self.flush.zero_()  # > L2: evict operands between steps
+        self.ops.gemm(self.A, self.B, bias=self.bias, epilogue=Epilogue.BIAS_RELU, out=self.C)
+
+    def launches_per_step(self):
+        return 1
+
+    def e2e_setup(self):
+        t = self.torch
+        self.hA, self.hB = self.A.cpu().pin_memory(), self.B.cpu().pin_memory()
+        self.hbias = self.bias.cpu().pin_memory()
+        self.hC = t.empty_like(self.C, device="cpu").pin_memory()
+        self.dA, self.dB, self.dbias = t.empty_like(self.A), t.empty_like(self.B), t.empty_like(self.bias)
+        self.h2d = (self.hA.numel() + self.hB.numel() + self.hbias.numel()) * 4
+        self.d2h = self.hC.numel() * 4
+
+    def e2e_step(self):
+        from paper_2603_06731_b200 import Epilogue
+        self.dA.copy_(self.hA, non_blocking=True)
+        self.dB.copy_(self.hB, non_blocking=True)
+        self.dbias.copy_(self.hbias, non_blocking=True)
+        self.ops.gemm(self.dA, self.dB, bias=self.dbias, epilogue=Epilogue.BIAS_RELU, out=self.C)
+        self.hC.copy_(self.C, non_blocking=True)
+
+    def reference_sample(self, threads):
+        return ReferenceGemmSample(self.n, threads, act="relu", rows=8, cols=128)
+
+
+WORKLOADS = {"gemm_bf16": lambda a: GemmBF16(a.size), "gemm_fp32": lambda a: GemmFP32()}
+
+
+# ======================================================= reference path ===
+
+def gemm_graph(m, n, k, act):
+    """matmul -> broadcast_in_dim(bias) -> add -> act in the unchanged graph
+    API (GELU = the 14-nest composite)."""
+    from oracle.graphs import matmul_epi_graph
+    g, fixed = matmul_epi_graph(m, n, k, act)
+    return g, fixed
+
+
+class ReferenceGemmSample:
+    """One bounded sample of the GEMM workload through the reference's CPU
+    path: af::lowerGraphToAffine + af::interpret (oracle/_ref), one
+    independent interpreter instance per host thread on its own
+    [rows x K] x [K x cols] shard (the interpreter is single-threaded and
+    safe across instances). Falls back to the oracle C port
+    (kind "port") when the reference build is absent."""
+
+    def __init__(self, K, threads, act="gelu", rows=2, cols=32):
+        import oracle as O
+        self.O = O
+        self.K, self.threads, self.rows, self.cols = K, threads, rows, cols
+        self.kind = "reference" if O.ref_available() else "port"
+        g, fixed = gemm_graph(rows, cols, K, act)
+        self.graph = json.dumps(g)
+        self.inputs = O.random_graph_inputs(g, 7, -1.0, 1.0)
+        self.inputs.update(fixed)
+        self.act = act
+        self.flops = 2.0 * rows * cols * K * threads
+
+    def describe(self):
+        how = ("af::lowerGraphToAffine + af::interpret (AffineForge reference, oracle/_ref)"
+               if self.kind == "reference" else "oracle C port (interp semantics)")
+        return (f"{self.threads} independent shards of [{self.rows}x{self.K}]x[{self.K}x{self.cols}]"
+                f" matmul+bias+{self.act} via {how}")
+
+    def run_once(self):
+        from concurrent.futures import ThreadPoolExecutor
+        O = self.O
+
+        def one(_):
+            if self.kind == "reference":
+                O.ref_run(self.graph, self.inputs, "interpret")
+            else:
+                ins = {k: O.round_to(v, O.F32) for k, v in self.inputs.items()}
+                epi = O.EPI_GELU_TANH if self.act == "gelu" else O.EPI_RELU
+                O.matmul(ins["a"], ins["b"], ins["bias"], epi=epi, interp=True, nthreads=1)
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            list(ex.map(one, range(self.threads)))
+        return time.perf_counter() - t0
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, wl, rank, world):
+    """--impl reference: the reference CPU path on the host cores."""
+    if rank != 0:
+        return 0
+    threads = host_threads()
+    sample = wl.reference_sample(threads)
+    for _ in range(args.warmup):
+        sample.run_once()
+    times = [sample.run_once() for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = sample.flops / t / 1e12
+    line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong" if isinstance(wl, GemmBF16) else "weak",
+            "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (makeRandomTensor)",
+            "config": wl.config(world), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": wl.unit, "cores": threads,
+                             "kind": sample.kind, "sample": sample.describe()},
+            "e2e": {"value": value, "unit": wl.unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ============================================================== afg arm ===
+
+def run_afg(args, wl, rank, world, local):
+    import torch
+
+    import paper_2603_06731_b200 as afg
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+    wl.setup(rank, world, dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        wl.step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = afg.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        wl.step()
+    ev1.record(stream)
+    barrier()
+    launches = afg.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop()
+    ms_max = max_over_ranks(ms)
+    value = wl.flops_total / (ms_max * 1e-3) / 1e12
+
+    # kernel-only duration of the dominant launch (same stream, events), for
+    # the roofline: one extra timed pass without anything else in the step
+    per = []
+    for _ in range(min(args.steps, 5)):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        wl.step() if not hasattr(wl, "kernel_only") else wl.kernel_only()
+        b.record(stream)
+        b.synchronize()
+        per.append(a.elapsed_time(b))
+    k_ms = statistics.median(per)
+    if wl.bound == "hbm":
+        achieved = wl.alg_bytes_rank / (k_ms * 1e-3) / 1e9
+        peak, unit = peaks["hbm_gbs"], "GB/s"
+    else:
+        achieved = wl.flops_rank / (k_ms * 1e-3) / 1e12
+        peak, unit = peaks["bf16_tflops"], "TFLOP/s"
+
+    # end to end through the C ABI with host buffers
+    wl.e2e_setup()
+    for _ in range(2):
+        wl.e2e_step()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e_steps = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(e_steps):
+        wl.e2e_step()
+    e1.record(stream)
+    barrier()
+    e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps)
+    e2e_value = wl.flops_total / (e_ms * 1e-3) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        sample = wl.reference_sample(threads)
+        t = sample.run_once()
+        cpu = {"value": sample.flops / t / 1e12, "unit": wl.unit, "cores": threads,
+               "kind": sample.kind, "sample": sample.describe(), "seconds": t}
+
+    if rank == 0:
+        line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
+                "higher_is_better": True,
+                "scaling": "strong" if isinstance(wl, GemmBF16) else "weak",
+                "vs_baseline": None, "dtype": wl.dtype,
+                "data": "synthetic (device-side makeRandomTensor stream, U[-1,1))",
+                "config": wl.config(world),
+                "roofline": {"bound": wl.bound if wl.bound in ("hbm", "tensor") else "tensor",
+                             "achieved": achieved, "peak": peak, "unit": unit,
+                             "frac": achieved / peak,
+                             "peak_source": f"{peaks['source']} (MEASURED_PEAKS.json burst)",
+                             "kernel_ms": k_ms, "traffic": traffic_for(wl.name)},
+                "e2e": {"value": e2e_value, "unit": wl.unit, "ms_per_step": e_ms,
+                        "h2d_bytes_per_step": wl.h2d * world, "d2h_bytes_per_step": wl.d2h * world,
+                        "path": "pinned host -> cudaMemcpyAsync -> afg C ABI -> D2H"},
+                "gpu_launches": int(launches),
+                "clocks": clk,
+                "cpu_baseline": cpu,
+                "impl": "afg"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="afg", choices=["afg", "reference"])
+    ap.add_argument("--workload", default="gemm_bf16", choices=sorted(WORKLOADS))
+    ap.add_argument("--size", type=int, default=16384)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    wl = WORKLOADS[args.workload](args)
+    if args.impl == "reference":
+        return run_reference(args, wl, rank, world)
+    return run_afg(args, wl, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

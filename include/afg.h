@@ -90,7 +90,11 @@ typedef enum afg_binop {
   AFG_OP_EXP = 4 /* unary: b ignored */
 } afg_binop;
 
-typedef enum afg_reduce_kind { AFG_REDUCE_SUM = 0, AFG_REDUCE_MAX = 1 } afg_reduce_kind;
+typedef enum afg_reduce_kind {
+  AFG_REDUCE_SUM = 0,
+  AFG_REDUCE_MAX = 1,
+  AFG_REDUCE_MAXABS = 2 /* max |x| (NaN-propagating) */
+} afg_reduce_kind;
 
 /* ------------------------------------------------------------ runtime --- */
 
@@ -167,6 +171,17 @@ AFG_API afg_status afg_attention_fwd(const void* q, const void* k, const void* v
                              int64_t Nq, int64_t Nk, int64_t D, float scale, int causal,
                              afg_dtype dtype, afg_dtype o_dtype, void* stream);
 
+/* Same with explicit element strides {seq, head, batch} for q, k, v and o
+ * (head_dim contiguous), e.g. reading Q/K/V straight out of a fused
+ * [B, S, 3, H, D] QKV projection and writing O as [B, S, H, D] (BERT).
+ * Tensor-core path only (f16/bf16, D in {64,128}, strides multiples of 8). */
+AFG_API afg_status afg_attention_fwd_strided(const void* q, const void* k, const void* v,
+                                     const float* bias, void* o, int64_t B, int64_t H,
+                                     int64_t Nq, int64_t Nk, int64_t D, float scale, int causal,
+                                     afg_dtype dtype, afg_dtype o_dtype, const int64_t* q_strides,
+                                     const int64_t* k_strides, const int64_t* v_strides,
+                                     const int64_t* o_strides, void* stream);
+
 /* ------------------------------------------------- memory-bound chains --- */
 
 /* Row softmax over the last axis (frontend.cpp:564-625 / oracles.cpp:175-190). */
@@ -191,6 +206,20 @@ AFG_API afg_status afg_reduce_lastdim(const void* x, void* out, int64_t rows, in
                               afg_reduce_kind kind, afg_dtype x_dtype, afg_dtype out_dtype,
                               void* stream);
 
+/* y = x broadcast into `out_shape`: input dim d maps to output dim dims[d]
+ * (broadcast_in_dim, frontend.cpp:489-500). */
+AFG_API afg_status afg_broadcast_in_dim(const void* x, void* y, int in_rank, const int64_t* in_shape,
+                                int out_rank, const int64_t* out_shape, const int64_t* dims,
+                                afg_dtype x_dtype, afg_dtype y_dtype, void* stream);
+
+/* Quantisation chain (interp.cpp quant/dequant; oracles.cpp:387-398):
+ *  mode 0 quantize  : y = clamp(round_half_away(x / scale), -128, 127)
+ *  mode 1 dequantize: y = x * scale
+ *  mode 2 / 3       : y = saturate(nearbyint(x)) to i8 / i32 (roundToType)
+ * Integer-typed tensors are carried exactly in f32 storage. */
+AFG_API afg_status afg_quantize(const void* x, void* y, int64_t n, float scale, int mode,
+                        afg_dtype x_dtype, afg_dtype y_dtype, void* stream);
+
 /* Dtype conversion (RNE), used by the graph executor's host staging. */
 AFG_API afg_status afg_convert(const void* x, void* y, int64_t n, afg_dtype x_dtype,
                        afg_dtype y_dtype, void* stream);
@@ -203,6 +232,48 @@ AFG_API afg_status afg_transpose(const void* x, void* y, int rank, const int64_t
  * u_i from splitmix64(seed, i), rounded (RNE) to `dtype`. */
 AFG_API afg_status afg_fill_uniform(void* x, int64_t n, uint64_t seed, float lo, float hi,
                             afg_dtype dtype, void* stream);
+
+/* --------------------------------------------------- encoder layer (BERT) --- */
+
+/* One post-LN transformer encoder layer (BERT-base: hidden 768, 12 heads,
+ * ffn 3072), x/y [batch*seq, hidden]; weights in the reference matmul layout
+ * W[K,N] (afg_gemm AFG_B_KN); biases / LN params fp32. Seven stream-ordered
+ * launches (see csrc/encoder.cpp); no allocation: `workspace` must hold
+ * afg_encoder_layer_workspace(...) bytes. */
+AFG_API size_t afg_encoder_layer_workspace(int64_t batch, int64_t seq, int64_t hidden,
+                                           int64_t ffn, afg_dtype dtype);
+AFG_API afg_status afg_encoder_layer_fwd(
+    const void* x, void* y, int64_t batch, int64_t seq, int64_t hidden, int64_t heads,
+    int64_t ffn, const void* w_qkv, const float* b_qkv, const void* w_o, const float* b_o,
+    const float* ln1_g, const float* ln1_b, const void* w_1, const float* b_1, const void* w_2,
+    const float* b_2, const float* ln2_g, const float* ln2_b, float eps, afg_dtype dtype,
+    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------ graph executor --- */
+
+/* The drop-in for the reference's parseGraphJson -> lowerGraphToAffine ->
+ * interpret path (frontend.cpp:57-113, :975; interp.cpp:690-696) for callers
+ * that cannot use the C++ API of afg_graph.h: executes the graph JSON on the
+ * current device with the given host inputs (values as doubles, keyed by
+ * tensor id with or without '%'; rounded to the declared element type on
+ * upload like the interpreter, interp.cpp:212-213) and returns the outputs
+ * keyed "%id" as doubles. fuse != 0 enables the fused kernel patterns.
+ * GraphError -> AFG_ERR_INVALID_ARG, InterpError -> AFG_ERR_CUDA. */
+typedef struct afg_graph_result afg_graph_result;
+AFG_API afg_status afg_graph_run(const char* graph_json, int n_inputs, const char* const* names,
+                         const double* const* data, const int64_t* numel, int fuse,
+                         void* stream, afg_graph_result** out);
+AFG_API int afg_graph_result_count(const afg_graph_result* r);
+AFG_API const char* afg_graph_result_name(const afg_graph_result* r, int i);
+AFG_API int afg_graph_result_rank(const afg_graph_result* r, int i);
+AFG_API int64_t afg_graph_result_dim(const afg_graph_result* r, int i, int d);
+AFG_API int64_t afg_graph_result_numel(const afg_graph_result* r, int i);
+AFG_API const double* afg_graph_result_data(const afg_graph_result* r, int i);
+/* One line per launched kernel (group): what the planner fused. */
+AFG_API const char* afg_graph_result_plan(const afg_graph_result* r);
+AFG_API void afg_graph_result_free(afg_graph_result* r);
+/* parseGraphJson + checkGraph only (GraphError -> AFG_ERR_INVALID_ARG). */
+AFG_API afg_status afg_graph_check_json(const char* graph_json);
 
 #ifdef __cplusplus
 }

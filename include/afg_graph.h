@@ -1,0 +1,104 @@
+// afg_graph.h - C++ host API mirroring the reference's graph/operator API
+// (AffineForge, /root/reference/proj/include/af/frontend.h:24-80 and
+// af/interp.h:29-125) on top of the afg C ABI (afg.h).
+//
+// A maintainer swaps executors in one line: where the reference test does
+//     af::Program p = af::lowerGraphToAffine(g, af::TargetConfig{});
+//     auto result = af::interpret(p, inputs);          // interp.h:97-100
+// the B200 path is
+//     auto outputs = afg::gpu::execute(g, inputs);      // same keys "%id"
+// with the same input contract (a value for every graph input, keyed "%id",
+// shape-checked) and the same outputs (declared outputs or produced-and-never-
+// consumed tensors, keyed "%id", values rounded to the declared element
+// type). Errors are the reference's: GraphError for malformed graphs /
+// unsupported ops / shape mismatches, InterpError for missing or mis-shaped
+// inputs and execution failures. See INTEGRATION.md for the adapter from the
+// reference's own af:: types.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace afg {
+namespace gpu {
+
+// af::ElementType order (ir.h:29) + BF16 (additive extension).
+enum class ElementType { F32 = 0, F16 = 1, I8 = 2, I32 = 3, BF16 = 10 };
+
+struct GraphError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InterpError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct TensorDesc {  // frontend.h:30-34
+  std::string id;
+  std::vector<int64_t> shape;
+  ElementType dtype = ElementType::F32;
+};
+
+struct TensorOpNode {  // frontend.h:36-50
+  std::string op;
+  std::vector<std::string> inputs;
+  std::string output;
+  std::vector<int64_t> perm;
+  std::vector<int64_t> dims;
+  int64_t strideY = 1, strideX = 1;
+  int64_t dilY = 1, dilX = 1;
+  bool samePadding = false;
+  bool transposed = false;
+  std::string reduceOp;
+  int64_t axis = -1;
+  double scale = 1.0;
+};
+
+struct TensorGraph {  // frontend.h:52-60
+  std::vector<TensorDesc> tensors;
+  std::vector<TensorOpNode> ops;
+  std::vector<std::string> outputs;
+  const TensorDesc* find(const std::string& id) const;
+  std::vector<std::string> inputIds() const;
+  std::vector<std::string> outputIds() const;
+};
+
+struct TensorValue {  // interp.h:33-44
+  std::vector<int64_t> shape;
+  ElementType type = ElementType::F32;
+  std::vector<double> data;
+  int64_t numElements() const {
+    int64_t n = 1;
+    for (int64_t d : shape) n *= d;
+    return n;
+  }
+};
+
+struct ConvGeometry {  // frontend.h:72-75
+  int64_t outH, outW, padY, padX;
+};
+
+TensorGraph parseGraphJson(const std::string& text);  // frontend.cpp:57-113
+void checkGraph(const TensorGraph& g);                  // frontend.cpp:264-294
+ConvGeometry convGeometry(int64_t inH, int64_t inW, int64_t kH, int64_t kW,
+                          const TensorOpNode& node);    // frontend.cpp:115-149
+
+struct GpuOptions {
+  void* stream = nullptr;  // cudaStream_t; NULL = legacy default stream
+  bool fuse = true;        // pattern-fuse matmul/conv epilogues and attention
+};
+
+struct ExecStats {
+  std::vector<std::string> plan;  // one line per launched kernel group
+  int fused = 0;                  // number of fused chains
+};
+
+// Executes the graph on the current CUDA device. inputs keyed "%id".
+std::map<std::string, TensorValue> execute(const TensorGraph& g,
+                                           const std::map<std::string, TensorValue>& inputs,
+                                           const GpuOptions& opt = {}, ExecStats* stats = nullptr);
+
+}  // namespace gpu
+}  // namespace afg

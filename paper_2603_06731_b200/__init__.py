@@ -66,6 +66,7 @@ class BinOp(IntEnum):
 class ReduceKind(IntEnum):
     SUM = 0
     MAX = 1
+    MAXABS = 2
 
 
 _P = ctypes.c_void_p
@@ -85,6 +86,11 @@ _SIGS = {
     "afg_conv2d_nchw": (_i, [_P, _P, _P] + [_I] * 13 + [_i, _I, _I, _i, _i, _P]),
     "afg_conv_pack_filter": (_i, [_P, _P, _I, _I, _I, _I, _i, _P]),
     "afg_attention_fwd": (_i, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _f, _i, _i, _i, _P]),
+    "afg_attention_fwd_strided": (_i, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _f, _i, _i, _i,
+                                       _P, _P, _P, _P, _P]),
+    "afg_encoder_layer_workspace": (ctypes.c_size_t, [_I, _I, _I, _I, _i]),
+    "afg_encoder_layer_fwd": (_i, [_P, _P, _I, _I, _I, _I, _I] + [_P] * 12 + [_f, _i, _P,
+                                                                             ctypes.c_size_t, _P]),
     "afg_softmax_lastdim": (_i, [_P, _P, _I, _I, _i, _i, _P]),
     "afg_layernorm_residual": (_i, [_P, _P, _P, _P, _P, _P, _I, _I, _f, _i, _P]),
     "afg_elementwise": (_i, [_P, _P, _P, _I, _I, _i, _i, _i, _i, _P]),
@@ -92,10 +98,20 @@ _SIGS = {
     "afg_convert": (_i, [_P, _P, _I, _i, _i, _P]),
     "afg_transpose": (_i, [_P, _P, _i, _P, _P, _i, _P]),
     "afg_fill_uniform": (_i, [_P, _I, ctypes.c_uint64, _f, _f, _i, _P]),
-    "afg_graph_execute_json": (_i, [ctypes.c_char_p, _i, ctypes.POINTER(ctypes.c_char_p),
-                                    ctypes.POINTER(_P), ctypes.POINTER(_I), _i,
-                                    ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_P),
-                                    ctypes.POINTER(_I), _P]),
+    "afg_broadcast_in_dim": (_i, [_P, _P, _i, _P, _i, _P, _P, _i, _i, _P]),
+    "afg_quantize": (_i, [_P, _P, _I, _f, _i, _i, _i, _P]),
+    "afg_graph_run": (_i, [ctypes.c_char_p, _i, ctypes.POINTER(ctypes.c_char_p),
+                           ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
+                           ctypes.POINTER(_I), _i, _P, ctypes.POINTER(_P)]),
+    "afg_graph_result_count": (_i, [_P]),
+    "afg_graph_result_name": (ctypes.c_char_p, [_P, _i]),
+    "afg_graph_result_rank": (_i, [_P, _i]),
+    "afg_graph_result_dim": (_I, [_P, _i, _i]),
+    "afg_graph_result_numel": (_I, [_P, _i]),
+    "afg_graph_result_data": (ctypes.POINTER(ctypes.c_double), [_P, _i]),
+    "afg_graph_result_plan": (ctypes.c_char_p, [_P]),
+    "afg_graph_result_free": (None, [_P]),
+    "afg_graph_check_json": (_i, [ctypes.c_char_p]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -137,3 +153,4 @@ def launch_count() -> int:
 
 
 from . import ops  # noqa: E402,F401  (torch-facing wrappers)
+from . import graph  # noqa: E402,F401  (graph executor binding)

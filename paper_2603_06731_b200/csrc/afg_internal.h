@@ -33,13 +33,28 @@ afg_status make_tmap(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
                      const uint64_t* dims, const uint64_t* strides_bytes,
                      const uint32_t* box, CUtensorMapSwizzle swz);
 
+// im2col descriptor over an NHWC tensor (dims C, W, H, N innermost first);
+// lower/upper = {W, H} bounding-box corners, traversal strides sw/sh.
+afg_status make_tmap_im2col_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
+                               int64_t C, int64_t W, int64_t H, int64_t N, const int* lower,
+                               const int* upper, int sw, int sh, int channels, int pixels);
+
 inline int dtype_bytes(afg_dtype t) { return t == AFG_F32 ? 4 : 2; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool valid_dtype(int t) { return t == AFG_F32 || t == AFG_F16 || t == AFG_BF16; }
+// AFG_OK iff a compute-capability-10.x device is current (no CPU fallback).
+afg_status check_device();
 
 // ---- kernel families (each .cu file) ---------------------------------------
 afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const float* bias,
                    const void* residual, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                    afg_dtype ab, afg_dtype c, afg_layout b_layout, afg_epilogue epi,
                    cudaStream_t stream);
+
+afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int64_t B,
+                   int64_t H, int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
+                   int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh, int64_t dw,
+                   int64_t OH, int64_t OW, afg_dtype dt, afg_epilogue epi, cudaStream_t stream);
 
 afg_status gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, const float* bias,
                      const void* residual, void* C, int64_t ldc, int64_t M, int64_t N,

@@ -27,6 +27,26 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
@@ -104,9 +124,32 @@ afg_status make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType 
   return make_tmap(map, base, dt, 2, dims, strides, box, swz);
 }
 
-namespace {
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+afg_status make_tmap_im2col_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
+                               int64_t C, int64_t W, int64_t H, int64_t N, const int* lower,
+                               const int* upper, int sw, int sh, int channels, int pixels) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  if (!fn) return set_error(AFG_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable (driver)");
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W),
+                              static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(N)};
+  const cuuint64_t es = 2;
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * es,
+                                 static_cast<cuuint64_t>(C * W) * es,
+                                 static_cast<cuuint64_t>(C * W * H) * es};
+  const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(sw), static_cast<cuuint32_t>(sh), 1};
+  CUresult r = fn(map, dt, 4, const_cast<void*>(base), dims, strides, lower, upper,
+                  static_cast<cuuint32_t>(channels), static_cast<cuuint32_t>(pixels), estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(AFG_ERR_INVALID_ARG, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
+  // Drivers up to 13.1 mis-encode a flag for tensors under 128 KiB (the same
+  // workaround CUTLASS applies, copy_traits_sm90_im2col.hpp).
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && C * W * H * N * static_cast<int64_t>(es) < 131072)
+    reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return AFG_OK;
+}
 
 afg_status check_device() {
   int dev = 0;
@@ -120,9 +163,6 @@ afg_status check_device() {
   return AFG_OK;
 }
 
-bool valid_dtype(int t) { return t == AFG_F32 || t == AFG_F16 || t == AFG_BF16; }
-
-}  // namespace
 }  // namespace afg
 
 using namespace afg;

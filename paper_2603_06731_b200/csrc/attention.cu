@@ -1,0 +1,528 @@
+// attention.cu - K3: the fused attention layer as ONE flash-style kernel.
+//
+// Reference: the attention graph transpose(k) -> batch_matmul(q, kt) ->
+// add(bias) -> softmax -> batch_matmul(soft, v) (test_frontend.cpp:275-305;
+// PAPER.md:371-378), whose reduce-reduce fusion with online-softmax
+// correction is a stub in the reference
+// (attention.cpp:1). This kernel realises the paper's three steps natively:
+//   rr-fusion      : the N x N score matrix never reaches HBM; running row max
+//                    m and denominator l, the output accumulator rescaled by
+//                    exp(m_old - m_new) (the paper's "correction", applied once
+//                    per KV tile, not per element: outline_matmuls);
+//   matmul outline : S = Q K^T and O += P V are separate tcgen05 MMAs into
+//                    TMEM (S double-buffered, O resident for the whole row
+//                    block);
+//   wmma fusion    : the softmax works on the S tile in registers
+//                    (tcgen05.ld), P goes to shared memory once as the A
+//                    operand of the PV MMA.
+// Extensions the BASELINE configs need: a scale on QK^T (the reference has
+// none; scale = 1 reproduces it) and causal masking (== the -inf upper-
+// triangular additive bias; causal KV tiles above the diagonal are skipped).
+//
+// CTA = one (b, h) and 128 query rows. Warps: 0 TMA, 1 MMA, 2 TMEM alloc,
+// 4-7 softmax/correction/epilogue (thread t owns query row t).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "afg_internal.h"
+#include "epilogue.cuh"
+#include "sm100.cuh"
+
+namespace afg {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;  // query rows per CTA
+constexpr int BN = 128;  // keys per KV tile
+constexpr int KV_STAGES = 2;
+
+struct AttnArgs {
+  const float* bias;  // [BH, Nq, Nk] or null
+  void* o;
+  int64_t o_ss, o_hs, o_bs;  // output strides (elements) of seq / head / batch
+  int BH, H, Nq, Nk;
+  float scale_log2;  // scale * log2(e)
+  int causal;
+  int o_dtype;
+};
+
+template <int D>
+struct AttnSmem {
+  static constexpr int TILE = BM * D * 2;  // Q / K / V tile bytes (BM == BN)
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + TILE;
+  static constexpr int V_OFF = K_OFF + KV_STAGES * TILE;
+  static constexpr int P_OFF = V_OFF + KV_STAGES * TILE;
+  static constexpr int P_BYTES = BM * BN * 2;
+  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  // bars: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2],
+  //       p_full, pv_done
+  static constexpr int NUM_BARS = 1 + 4 * KV_STAGES + 4 + 2;
+  static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, bool bf16) {
+  return bf16 ? pack_bf16(a, b) : pack_f16(a, b);
+}
+
+template <int D, bool BF16>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                    const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const AttnArgs args) {
+  using L = AttnSmem<D>;
+  constexpr int DB = D / 64;  // 128-byte swizzle atoms per row of Q/K/V
+  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t O_COL = 2 * BN;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + KV_STAGES;
+  uint64_t* v_full = k_empty + KV_STAGES;
+  uint64_t* v_empty = v_full + KV_STAGES;
+  uint64_t* s_full = v_empty + KV_STAGES;
+  uint64_t* s_free = s_full + 2;
+  uint64_t* p_full = s_free + 2;
+  uint64_t* pv_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  // heavy causal tiles first: reverse the q-tile order
+  const int n_qtiles = (args.Nq + BM - 1) / BM;
+  const int qt = n_qtiles - 1 - static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y;
+  const int hh = bh % args.H;
+  const int bb = bh / args.H;
+  const int q0 = qt * BM;
+  int n_kv = (args.Nk + BN - 1) / BN;
+  if (args.causal) n_kv = min(n_kv, (q0 + BM - 1) / BN + 1);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KV_STAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // --------------------------------------------------------------- TMA --
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, L::TILE);
+      for (int a = 0; a < DB; ++a)
+        tma_load_4d(smem + L::Q_OFF + a * (BM * 128), &tmQ, q_full, a * 64, q0, hh, bb);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % KV_STAGES;
+        const uint32_t ph = (j / KV_STAGES) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], L::TILE);
+        for (int a = 0; a < DB; ++a)
+          tma_load_4d(smem + L::K_OFF + st * L::TILE + a * (BN * 128), &tmK, &k_full[st], a * 64,
+                      j * BN, hh, bb);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], L::TILE);
+        for (int a = 0; a < DB; ++a)
+          tma_load_4d(smem + L::V_OFF + st * L::TILE + a * (BN * 128), &tmV, &v_full[st], a * 64,
+                      j * BN, hh, bb);
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------------- MMA --
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_f16(BM, BN, BF16 ? 1u : 0u, 0u, 0u);
+      constexpr uint32_t idesc_o = idesc_f16(BM, D, BF16 ? 1u : 0u, 0u, 1u);
+      const uint32_t q_addr = smem_u32(smem + L::Q_OFF);
+      const uint32_t p_addr = smem_u32(smem + L::P_OFF);
+      auto issue_s = [&](int j) {
+        const int st = j % KV_STAGES;
+        const int sb = j & 1;
+        if (j >= 2) mbar_wait(&s_free[sb], ((j - 2) >> 1) & 1);
+        mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(smem + L::K_OFF + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * (BM * 128) + (kk % 4) * 32;
+          mma_f16_ss(tmem + sb * BN, desc_kmajor_sw128(q_addr + off),
+                     desc_kmajor_sw128(k_addr + (kk / 4) * (BN * 128) + (kk % 4) * 32), idesc_s,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[sb]);
+        mma_commit(&k_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        const int st = j % KV_STAGES;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(smem + L::V_OFF + st * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t a = desc_kmajor_sw128(p_addr + (kk / 4) * (BM * 128) + (kk % 4) * 32);
+          const uint64_t b = desc_mnmajor_sw128(v_addr + kk * 16 * 128, BN * 128);
+          mma_f16_ss(tmem + O_COL, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(pv_done);
+        mma_commit(&v_empty[st]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------ softmax / correction / out --
+    const int w4 = warp - 4;
+    const int row = w4 * 32 + lane;  // query row within the tile == TMEM lane
+    const int qi = q0 + row;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
+    const uint32_t p_row = smem_u32(smem + L::P_OFF) + row * 128;
+    const float* brow =
+        args.bias ? args.bias + (static_cast<int64_t>(bh) * args.Nq + min(qi, args.Nq - 1)) *
+                                    args.Nk
+                  : nullptr;
+    float m = -INFINITY;  // running max, in scaled log2 units
+    float l = 0.0f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(lane_base + sb * BN + c * 32, sr[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_free[sb]);
+      // scale, bias, masks; row max
+      const int k0 = j * BN;
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int kj = k0 + c * 32 + e;
+          float v = __uint_as_float(sr[c][e]) * args.scale_log2;
+          if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
+          if (kj >= args.Nk || (args.causal && kj > qi)) v = -INFINITY;
+          sr[c][e] = __float_as_uint(v);
+          tmax = fmaxf(tmax, v);
+        }
+      }
+      const float m_new = fmaxf(m, tmax);
+      const float base = m_new == -INFINITY ? 0.0f : m_new;
+      const float alpha = ex2(m - base);  // 0 on the first tile (m = -inf)
+      float tsum = 0.0f;
+      uint32_t pk[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = ex2(__uint_as_float(sr[c][2 * e]) - base);
+          const float p1 = ex2(__uint_as_float(sr[c][2 * e + 1]) - base);
+          tsum += p0 + p1;
+          pk[c][e] = pack2(p0, p1, BF16);
+        }
+      }
+      l = l * alpha + tsum;
+      // P buffer and O are owned by the PV MMA of the previous tile
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        // correction O *= exp(m_old - m_new), once per tile. tcgen05.ld/st are
+        // warp-collective: the decision must be warp-uniform (rows whose max
+        // did not move scale by alpha == 1).
+        if (__any_sync(0xffffffffu, m_new > m)) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(lane_base + O_COL + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(lane_base + O_COL + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      m = m_new;
+      // P (row `row`, 128 keys) -> smem, K-major SWIZZLE_128B, 2 atoms of 64 keys
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int key_chunk = c * 4 + q;  // 16-byte chunk of 8 keys, 0..15
+          const int atom = key_chunk / 8;
+          const int ch = key_chunk % 8;
+          const uint32_t addr = p_row + atom * (BM * 128) + ((ch ^ (row & 7)) * 16);
+          st_shared_v4(addr, pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // ---- epilogue: O / l -> global
+    mbar_wait(pv_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+    const bool valid = qi < args.Nq;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(lane_base + O_COL + c * 32, o);
+      tmem_wait_ld();
+      if (!valid) continue;
+      const int64_t base_idx = static_cast<int64_t>(bb) * args.o_bs +
+                               static_cast<int64_t>(hh) * args.o_hs +
+                               static_cast<int64_t>(qi) * args.o_ss + c * 32;
+      if (args.o_dtype == AFG_F32) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + base_idx);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
+                               __uint_as_float(o[4 * v + 2]) * inv_l,
+                               __uint_as_float(o[4 * v + 3]) * inv_l);
+      } else {
+        const bool ob = args.o_dtype == AFG_BF16;
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + base_idx);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 u;
+          u.x = pack2(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l, ob);
+          u.y = pack2(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l, ob);
+          u.z = pack2(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l, ob);
+          u.w = pack2(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l, ob);
+          dst[v] = u;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem);
+  }
+}
+
+// ----------------------------------------------------------- SIMT fallback --
+// Any D / dtype / length: one CTA per (bh, query row); scores staged in smem.
+template <typename T>
+__global__ void attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                 const T* __restrict__ v, const float* __restrict__ bias,
+                                 void* __restrict__ o, int Nq, int Nk, int D, float scale,
+                                 int causal, int o_dtype) {
+  extern __shared__ float sc[];  // Nk scores + 32 reduction slots
+  float* red = sc + Nk;
+  const int i = blockIdx.x;
+  const int64_t bh = blockIdx.y;
+  const T* qr = q + (bh * Nq + i) * D;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < Nk; j += blockDim.x) {
+    const T* kr = k + (bh * Nk + j) * D;
+    float acc = 0.0f;
+    for (int d = 0; d < D; ++d) acc = fmaf(OutCvt<T>::from(qr[d]), OutCvt<T>::from(kr[d]), acc);
+    acc *= scale;
+    if (bias) acc += bias[(bh * Nq + i) * Nk + j];
+    if (causal && j > i) acc = -INFINITY;
+    sc[j] = acc;
+    mx = fmaxf(mx, acc);
+  }
+  for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int w = 0; w < blockDim.x / 32; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  const float base = mx == -INFINITY ? 0.0f : mx;
+  float sum = 0.0f;
+  for (int j = threadIdx.x; j < Nk; j += blockDim.x) {
+    const float e = expf(sc[j] - base);
+    sc[j] = e;
+    sum += e;
+  }
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = sum;
+  __syncthreads();
+  sum = 0.0f;
+  for (int w = 0; w < blockDim.x / 32; ++w) sum += red[w];
+  const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.0f;
+    for (int j = 0; j < Nk; ++j) acc = fmaf(sc[j], OutCvt<T>::from(v[(bh * Nk + j) * D + d]), acc);
+    acc *= inv;
+    const int64_t idx = (bh * Nq + i) * D + d;
+    if (o_dtype == AFG_F32)
+      reinterpret_cast<float*>(o)[idx] = acc;
+    else if (o_dtype == AFG_F16)
+      reinterpret_cast<__half*>(o)[idx] = __float2half_rn(acc);
+    else
+      reinterpret_cast<__nv_bfloat16*>(o)[idx] = __float2bfloat16_rn(acc);
+  }
+}
+
+template <int D, bool BF16>
+cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                      const AttnArgs& a, cudaStream_t s) {
+  auto kern = attn_fwd_kernel<D, BF16>;
+  constexpr int smem = AttnSmem<D>::TOTAL;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((a.Nq + BM - 1) / BM, a.BH);
+  kern<<<grid, 256, smem, s>>>(tq, tk, tv, a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace afg
+
+using namespace afg;
+
+namespace afg {
+namespace {
+
+// Strides in elements: s = sequence row, h = head, b = batch (d is unit).
+struct Strides {
+  int64_t s, h, b;
+};
+
+afg_status attention_core(const void* q, const void* k, const void* v, const float* bias, void* o,
+                          int64_t B, int64_t H, int64_t Nq, int64_t Nk, int64_t D, float scale,
+                          int causal, afg_dtype dt, afg_dtype od, Strides sq, Strides sk,
+                          Strides sv, Strides so, bool contiguous, cudaStream_t s) {
+  if (!q || !k || !v || !o) return set_error(AFG_ERR_INVALID_ARG, "afg_attention_fwd: null operand");
+  if (B <= 0 || H <= 0 || Nq <= 0 || Nk <= 0 || D <= 0)
+    return set_error(AFG_ERR_INVALID_ARG, "afg_attention_fwd: non-positive extent");
+  if (!valid_dtype(dt) || !valid_dtype(od))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_attention_fwd: bad dtype");
+  const int64_t BH = B * H;
+  if (BH > 65535 || Nq >= (1 << 30) || Nk >= (1 << 30))
+    return set_error(AFG_ERR_UNSUPPORTED, "afg_attention_fwd: extent too large");
+  afg_status st = check_device();
+  if (st != AFG_OK) return st;
+  const bool strides_ok = (sq.s % 8 == 0) && (sq.h % 8 == 0) && (sq.b % 8 == 0) &&
+                          (sk.s % 8 == 0) && (sk.h % 8 == 0) && (sk.b % 8 == 0) &&
+                          (sv.s % 8 == 0) && (sv.h % 8 == 0) && (sv.b % 8 == 0);
+  const bool tc = (dt == AFG_F16 || dt == AFG_BF16) && (D == 64 || D == 128) && aligned16(q) &&
+                  aligned16(k) && aligned16(v) && aligned16(o) && strides_ok &&
+                  (so.s % 8 == 0) && (so.h % 8 == 0) && (so.b % 8 == 0);
+  if (tc) {
+    const CUtensorMapDataType tdt =
+        dt == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUtensorMap tq, tk, tv;
+    const uint32_t box[4] = {64, 128, 1, 1};
+    auto map4 = [&](CUtensorMap* m, const void* base, int64_t N, Strides str) {
+      const uint64_t dims[4] = {static_cast<uint64_t>(D), static_cast<uint64_t>(N),
+                                static_cast<uint64_t>(H), static_cast<uint64_t>(B)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(str.s) * 2,
+                                   static_cast<uint64_t>(str.h) * 2,
+                                   static_cast<uint64_t>(str.b) * 2};
+      return make_tmap(m, base, tdt, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    };
+    if ((st = map4(&tq, q, Nq, sq)) != AFG_OK) return st;
+    if ((st = map4(&tk, k, Nk, sk)) != AFG_OK) return st;
+    if ((st = map4(&tv, v, Nk, sv)) != AFG_OK) return st;
+    AttnArgs a;
+    a.bias = bias;
+    a.o = o;
+    a.o_ss = so.s;
+    a.o_hs = so.h;
+    a.o_bs = so.b;
+    a.BH = static_cast<int>(BH);
+    a.H = static_cast<int>(H);
+    a.Nq = static_cast<int>(Nq);
+    a.Nk = static_cast<int>(Nk);
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.causal = causal;
+    a.o_dtype = od;
+    cudaError_t e;
+    if (D == 128)
+      e = dt == AFG_BF16 ? launch_tc<128, true>(tq, tk, tv, a, s) : launch_tc<128, false>(tq, tk, tv, a, s);
+    else
+      e = dt == AFG_BF16 ? launch_tc<64, true>(tq, tk, tv, a, s) : launch_tc<64, false>(tq, tk, tv, a, s);
+    return cuda_status(e, "attention tc launch");
+  }
+  if (!contiguous)
+    return set_error(AFG_ERR_UNSUPPORTED, "strided attention needs the tensor-core path "
+                     "(f16/bf16, D in {64,128}, 16-byte strides)");
+  const size_t smem = (static_cast<size_t>(Nk) + 32) * sizeof(float);
+  if (smem > 200 * 1024) return set_error(AFG_ERR_UNSUPPORTED, "attention SIMT path: Nk too large");
+  dim3 grid(static_cast<unsigned>(Nq), static_cast<unsigned>(BH));
+#define AFG_ATT(T)                                                                              \
+  do {                                                                                          \
+    cudaFuncSetAttribute(attn_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                         static_cast<int>(smem));                                               \
+    attn_simt_kernel<T><<<grid, 128, smem, s>>>(                                                \
+        reinterpret_cast<const T*>(q), reinterpret_cast<const T*>(k),                           \
+        reinterpret_cast<const T*>(v), bias, o, (int)Nq, (int)Nk, (int)D, scale, causal, (int)od); \
+  } while (0)
+  if (dt == AFG_F32) AFG_ATT(float);
+  else if (dt == AFG_F16) AFG_ATT(__half);
+  else AFG_ATT(__nv_bfloat16);
+#undef AFG_ATT
+  count_launch();
+  return cuda_status(cudaGetLastError(), "attention simt launch");
+}
+
+}  // namespace
+}  // namespace afg
+
+extern "C" afg_status afg_attention_fwd(const void* q, const void* k, const void* v,
+                                        const float* bias, void* o, int64_t B, int64_t H,
+                                        int64_t Nq, int64_t Nk, int64_t D, float scale,
+                                        int causal, afg_dtype dt, afg_dtype od, void* stream) {
+  const Strides sq{D, Nq * D, H * Nq * D}, sk{D, Nk * D, H * Nk * D};
+  return attention_core(q, k, v, bias, o, B, H, Nq, Nk, D, scale, causal, dt, od, sq, sk, sk, sq,
+                        true, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" afg_status afg_attention_fwd_strided(
+    const void* q, const void* k, const void* v, const float* bias, void* o, int64_t B,
+    int64_t H, int64_t Nq, int64_t Nk, int64_t D, float scale, int causal, afg_dtype dt,
+    afg_dtype od, const int64_t* q_strides, const int64_t* k_strides, const int64_t* v_strides,
+    const int64_t* o_strides, void* stream) {
+  if (!q_strides || !k_strides || !v_strides || !o_strides)
+    return set_error(AFG_ERR_INVALID_ARG, "afg_attention_fwd_strided: null strides");
+  auto S = [](const int64_t* p) { return Strides{p[0], p[1], p[2]}; };
+  return attention_core(q, k, v, bias, o, B, H, Nq, Nk, D, scale, causal, dt, od, S(q_strides),
+                        S(k_strides), S(v_strides), S(o_strides), false,
+                        static_cast<cudaStream_t>(stream));
+}

@@ -365,11 +365,18 @@ __global__ void reduce_kernel(const void* __restrict__ x, void* __restrict__ out
   const int lane = threadIdx.x % 32;
   if (row >= rows) return;
   float acc = kind == AFG_REDUCE_MAX ? -INFINITY : 0.0f;
+  bool nan = false;
   for (int64_t c = lane; c < cols; c += 32) {
     const float v = ld_any(x, row * cols + c, xdt);
-    acc = kind == AFG_REDUCE_MAX ? fmaxf(acc, v) : acc + v;
+    if (kind == AFG_REDUCE_MAXABS) {
+      nan |= isnan(v);
+      acc = fmaxf(acc, fabsf(v));
+    } else {
+      acc = kind == AFG_REDUCE_MAX ? fmaxf(acc, v) : acc + v;
+    }
   }
-  acc = kind == AFG_REDUCE_MAX ? warp_max(acc) : warp_sum(acc);
+  acc = kind == AFG_REDUCE_SUM ? warp_sum(acc) : warp_max(acc);
+  if (kind == AFG_REDUCE_MAXABS && __any_sync(0xffffffffu, nan)) acc = NAN;
   if (lane == 0) st_any(out, row, odt, acc);
 }
 
@@ -378,6 +385,45 @@ __global__ void convert_kernel(const void* __restrict__ x, void* __restrict__ y,
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     st_any(y, i, ydt, ld_any(x, i, xdt));
+}
+
+struct BroadcastArgs {
+  int out_rank;
+  int64_t out_shape[6];
+  int64_t in_stride_for_out[6];  // 0 for broadcast output dims
+};
+
+__global__ void broadcast_kernel(const void* __restrict__ x, void* __restrict__ y, int64_t n,
+                                 BroadcastArgs b, int xdt, int ydt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t rem = i, src = 0;
+    for (int d = b.out_rank - 1; d >= 0; --d) {
+      const int64_t idx = rem % b.out_shape[d];
+      rem /= b.out_shape[d];
+      src += idx * b.in_stride_for_out[d];
+    }
+    st_any(y, i, ydt, ld_any(x, src, xdt));
+  }
+}
+
+__global__ void quantize_kernel(const void* __restrict__ x, void* __restrict__ y, int64_t n,
+                                float scale, int mode, int xdt, int ydt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = ld_any(x, i, xdt);
+    float r;
+    if (mode == 0) {
+      r = fminf(fmaxf(roundf(v / scale), -128.0f), 127.0f);  // std::round: half away from 0
+    } else if (mode == 1) {
+      r = v * scale;
+    } else if (mode == 2) {
+      r = fminf(fmaxf(rintf(v), -128.0f), 127.0f);
+    } else {
+      r = fminf(fmaxf(rintf(v), -2147483648.0f), 2147483647.0f);
+    }
+    st_any(y, i, ydt, r);
+  }
 }
 
 struct TransposeArgs {
@@ -508,6 +554,45 @@ afg_status afg_reduce_lastdim(const void* x, void* out, int64_t rows, int64_t co
                                                                      xd, od);
   count_launch();
   return cuda_status(cudaGetLastError(), "reduce launch");
+}
+
+afg_status afg_broadcast_in_dim(const void* x, void* y, int in_rank, const int64_t* in_shape,
+                                int out_rank, const int64_t* out_shape, const int64_t* dims,
+                                afg_dtype xd, afg_dtype yd, void* stream) {
+  if (!x || !y || !out_shape || out_rank <= 0 || out_rank > 6 || in_rank < 0 ||
+      in_rank > out_rank || (in_rank > 0 && (!in_shape || !dims)) || !valid_dt(xd) ||
+      !valid_dt(yd))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_broadcast_in_dim: bad arguments");
+  BroadcastArgs b;
+  b.out_rank = out_rank;
+  int64_t n = 1;
+  for (int d = 0; d < out_rank; ++d) {
+    b.out_shape[d] = out_shape[d];
+    b.in_stride_for_out[d] = 0;
+    n *= out_shape[d];
+  }
+  int64_t st = 1;
+  for (int d = in_rank - 1; d >= 0; --d) {
+    if (dims[d] < 0 || dims[d] >= out_rank || out_shape[dims[d]] != in_shape[d])
+      return set_error(AFG_ERR_INVALID_ARG, "afg_broadcast_in_dim: dims/extents mismatch");
+    b.in_stride_for_out[dims[d]] = st;
+    st *= in_shape[d];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  broadcast_kernel<<<grid_for(n), 256, 0, s>>>(x, y, n, b, xd, yd);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "broadcast launch");
+}
+
+afg_status afg_quantize(const void* x, void* y, int64_t n, float scale, int mode, afg_dtype xd,
+                        afg_dtype yd, void* stream) {
+  if (!x || !y || n <= 0 || mode < 0 || mode > 3 || (mode == 0 && scale == 0.0f) ||
+      !valid_dt(xd) || !valid_dt(yd))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_quantize: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  quantize_kernel<<<grid_for(n), 256, 0, s>>>(x, y, n, scale, mode, xd, yd);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "quantize launch");
 }
 
 afg_status afg_convert(const void* x, void* y, int64_t n, afg_dtype xd, afg_dtype yd,

@@ -47,6 +47,9 @@ struct GemmTcArgs {
   void* C;
   int num_m_blocks, num_n_blocks;
   int epi;
+  // implicit-GEMM conv (IM2COL): output pixel m = (n, p, q) over OH x OW,
+  // K = KH*KW*C ordered (ky, kx, c) like the OHWI filter.
+  int c_blocks, KW, dil_w, dil_h, OH, OW, stride_w, stride_h, lower_w, lower_h;
 };
 
 template <int BLOCK_N, int STAGES>
@@ -143,7 +146,7 @@ __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], cons
   }
 }
 
-template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT>
+template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT, bool IM2COL>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const GemmTcArgs args) {
@@ -203,7 +206,22 @@ __global__ void __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], L::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full_bar[stage], kb * BLOCK_K, mb * BLOCK_M);
+          if constexpr (IM2COL) {
+            const int m0 = mb * BLOCK_M;
+            const int q = m0 % args.OW;
+            const int p = (m0 / args.OW) % args.OH;
+            const int n = m0 / (args.OW * args.OH);
+            const int tap = kb / args.c_blocks;
+            const int cb = kb - tap * args.c_blocks;
+            const int ky = tap / args.KW;
+            const int kx = tap - ky * args.KW;
+            tma_load_im2col_4d(sa, &tmA, &full_bar[stage], cb * BLOCK_K,
+                               args.lower_w + q * args.stride_w, args.lower_h + p * args.stride_h,
+                               n, static_cast<uint16_t>(kx * args.dil_w),
+                               static_cast<uint16_t>(ky * args.dil_h));
+          } else {
+            tma_load_2d(sa, &tmA, &full_bar[stage], kb * BLOCK_K, mb * BLOCK_M);
+          }
           if constexpr (B_MN_MAJOR) {
 #pragma unroll
             for (int j = 0; j < BLOCK_N / 64; ++j)
@@ -293,10 +311,11 @@ __global__ void __launch_bounds__(256, 1)
 
 // --------------------------------------------------------------- host side --
 
-template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT>
+template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT,
+          bool IM2COL = false>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmTcArgs& args, cudaStream_t stream) {
-  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT>;
+  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL>;
   constexpr int smem = SmemLayout<BLOCK_N, STAGES>::TOTAL;
   static bool configured = false;  // per-instantiation, per-process
   if (!configured) {
@@ -372,6 +391,72 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   if (e == cudaErrorNotSupported)
     return set_error(AFG_ERR_UNSUPPORTED, "gemm_tc: unsupported (ab, c) dtype pair");
   return cuda_status(e, "gemm_tc launch");
+}
+
+// Implicit-GEMM convolution on the same pipeline: the A tile of 128 output
+// pixels x 64 channels for filter tap (ky, kx) is gathered by the TMA unit in
+// im2col mode (zero fill outside the padded bounding box), B is the OHWI
+// filter viewed as [OC, KH*KW*C] (K-major). SPEC.md:388-452 (conv_gemm.cpp is
+// a stub in the reference).
+afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int64_t B,
+                   int64_t H, int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
+                   int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh, int64_t dw,
+                   int64_t OH, int64_t OW, afg_dtype dt, afg_epilogue epi, cudaStream_t stream) {
+  const int64_t M = B * OH * OW;
+  const int64_t K = KH * KW * C;
+  const int block_n = OC >= 256 ? 256 : (OC > 64 ? 128 : 64);
+  const CUtensorMapDataType tdt =
+      dt == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  // padded bounding box: lower = -pad_begin, upper = pad_end - (K-1)*dil with
+  // pad_end chosen so that the traversal yields exactly OH x OW positions.
+  const int64_t pb = (OH - 1) * sh + (KH - 1) * dh + 1 - H - pt;
+  const int64_t pr = (OW - 1) * sw + (KW - 1) * dw + 1 - W - pl;
+  const int lower[2] = {static_cast<int>(-pl), static_cast<int>(-pt)};
+  const int upper[2] = {static_cast<int>(pr - (KW - 1) * dw), static_cast<int>(pb - (KH - 1) * dh)};
+  for (int i = 0; i < 2; ++i)
+    if (lower[i] < -128 || lower[i] > 127 || upper[i] < -128 || upper[i] > 127)
+      return set_error(AFG_ERR_UNSUPPORTED, "conv_tc: padding outside the im2col corner range");
+  if (sh > 8 || sw > 8) return set_error(AFG_ERR_UNSUPPORTED, "conv_tc: stride > 8");
+  CUtensorMap tmA, tmB;
+  afg_status st = make_tmap_im2col_4d(&tmA, x, tdt, C, W, H, B, lower, upper,
+                                      static_cast<int>(sw), static_cast<int>(sh), BLOCK_K, BLOCK_M);
+  if (st != AFG_OK) return st;
+  st = make_tmap_2d(&tmB, w, tdt, 2, K, OC, K, BLOCK_K, block_n);
+  if (st != AFG_OK) return st;
+  GemmTcArgs args{};
+  args.M = static_cast<int>(M);
+  args.N = static_cast<int>(OC);
+  args.K = static_cast<int>(K);
+  args.ldc = static_cast<int>(OC);
+  args.bias = bias;
+  args.residual = nullptr;
+  args.C = y;
+  args.num_m_blocks = static_cast<int>((M + BLOCK_M - 1) / BLOCK_M);
+  args.num_n_blocks = static_cast<int>((OC + block_n - 1) / block_n);
+  args.epi = static_cast<int>(epi);
+  args.c_blocks = static_cast<int>(C / BLOCK_K);
+  args.KW = static_cast<int>(KW);
+  args.dil_w = static_cast<int>(dw);
+  args.dil_h = static_cast<int>(dh);
+  args.OH = static_cast<int>(OH);
+  args.OW = static_cast<int>(OW);
+  args.stride_w = static_cast<int>(sw);
+  args.stride_h = static_cast<int>(sh);
+  args.lower_w = lower[0];
+  args.lower_h = lower[1];
+  cudaError_t e;
+#define AFG_CONV_V(BN, ST)                                                                  \
+  (dt == AFG_BF16 ? launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, args, \
+                                                                            stream)         \
+                  : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, args, stream))
+  if (block_n == 256)
+    e = AFG_CONV_V(256, 4);
+  else if (block_n == 128)
+    e = AFG_CONV_V(128, 6);
+  else
+    e = AFG_CONV_V(64, 8);
+#undef AFG_CONV_V
+  return cuda_status(e, "conv_tc launch");
 }
 
 }  // namespace afg

@@ -1,0 +1,126 @@
+"""GPU parity of K1 (tcgen05 bf16/fp16 GEMM + fused epilogue) and K1b (fp32
+SIMT GEMM) against the oracle restatement of the reference path.
+
+Tolerances (the reference's rule |a-b| <= tol * max(|a|,|b|,1),
+interp.cpp:698-730):
+  * fp32 GEMM vs the interpreter restatement (sequential f32-rounded FMA,
+    interp.cpp:335-347): bit-exact (tol 0); vs the double oracle
+    (matmulReference, oracles.cpp:122-134): 1e-4 (BASELINE north star).
+  * bf16/fp16 inputs, fp32 output, vs the double oracle on the same rounded
+    inputs: 1e-5 * max(1, K/1024) (fp32 accumulation-order error).
+  * bf16/fp16 output: one output ulp, 2^-7 (bf16) / 2^-10 (fp16), against the
+    oracle result rounded to the output type.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2603_06731_b200 import Epilogue, Layout, ops
+from tests.gpu_util import check, seeded, to_host
+
+pytestmark = pytest.mark.gpu
+
+EPI = {Epilogue.NONE: O.EPI_NONE, Epilogue.BIAS: O.EPI_BIAS, Epilogue.BIAS_RELU: O.EPI_RELU,
+       Epilogue.BIAS_GELU_TANH: O.EPI_GELU_TANH, Epilogue.BIAS_GELU_ERF: O.EPI_GELU_ERF}
+ULP = {torch.bfloat16: 2.0**-7, torch.float16: 2.0**-10}
+
+
+def run_case(cuda, M, N, K, dt=torch.bfloat16, out=None, epi=Epilogue.BIAS_GELU_TANH,
+             layout=Layout.B_KN, residual=False, seed=5, rows=None):
+    out = out or dt
+    a, ah = seeded((M, K), "a", seed, dtype=dt)
+    bshape = (K, N) if layout == Layout.B_KN else (N, K)
+    b, bh = seeded(bshape, "b", seed, dtype=dt)
+    bias, biash = seeded((N,), "bias", seed, dtype=torch.float32)
+    res = resh = None
+    if residual:
+        res, resh = seeded((M, N), "res", seed, dtype=out)
+    c = ops.gemm(a, b, bias=bias if epi != Epilogue.NONE else None, epilogue=epi,
+                 out_dtype=out, b_layout=layout, residual=res)
+    torch.cuda.synchronize()
+    got = to_host(c)
+    if rows is not None:
+        got = got[rows]
+    out_code = O.F32 if out == torch.float32 else (O.BF16 if out == torch.bfloat16 else O.F16)
+    # fp32 accumulation then the epilogue in double, rounded to the output type
+    acc = O.matmul(ah, bh, biash, epi=EPI[epi], out_t=O.F64, b_nk=layout == Layout.B_NK,
+                   rows=rows)
+    if residual:
+        acc = acc + (resh if rows is None else resh[rows])
+    want = O.round_to(acc, out_code)
+    tol = ULP[out] if out in ULP else 1e-5 * max(1.0, K / 1024)
+    return check(got, want, tol, f"gemm {M}x{N}x{K} {dt}->{out} epi={int(epi)}")
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (100, 200, 72),
+                                   (333, 130, 200), (1024, 1024, 1024), (257, 768, 768),
+                                   (64, 64, 64), (2048, 2048, 512)])
+def test_bf16_gelu_shapes(cuda, M, N, K):
+    run_case(cuda, M, N, K)
+
+
+@pytest.mark.parametrize("epi", list(Epilogue))
+def test_bf16_epilogues_fp32_out(cuda, epi):
+    run_case(cuda, 384, 320, 256, out=torch.float32, epi=epi)
+
+
+def test_fp16_relu_fp16_out(cuda):
+    run_case(cuda, 512, 512, 384, dt=torch.float16, epi=Epilogue.BIAS_RELU)
+
+
+def test_b_nk_layout(cuda):
+    run_case(cuda, 512, 384, 256, layout=Layout.B_NK)
+    run_case(cuda, 300, 64, 128, layout=Layout.B_NK, epi=Epilogue.BIAS)
+
+
+def test_residual_epilogue(cuda):
+    run_case(cuda, 512, 768, 768, epi=Epilogue.BIAS, residual=True)
+
+
+def test_large_k_fp32_out(cuda):
+    run_case(cuda, 256, 256, 8192, out=torch.float32, epi=Epilogue.BIAS)
+
+
+def test_full_size_sampled_rows_4096(cuda):
+    # BASELINE configs[1] shape class at full size, parity on sampled rows
+    rows = np.array([0, 1, 127, 128, 2047, 2048, 4000, 4095])
+    run_case(cuda, 4096, 4096, 4096, rows=rows)
+
+
+# ------------------------------------------------------------------- fp32 ---
+
+def test_fp32_config1_bit_exact_vs_interpreter(cuda):
+    """BASELINE configs[0]: fp32 1024^3 + bias + ReLU, the reference's own
+    matmul->broadcast_in_dim->add->max graph. Sequential fp32 FMA == the
+    interpreter's double FMA rounded to f32 at every store."""
+    n = 1024
+    a, ah = seeded((n, n), "a", 1, dtype=torch.float32)
+    b, bh = seeded((n, n), "b", 2, dtype=torch.float32)
+    bias, biash = seeded((n,), "bias", 3, dtype=torch.float32)
+    c = ops.gemm(a, b, bias=bias, epilogue=Epilogue.BIAS_RELU)
+    got = to_host(c)
+    want_interp = O.matmul(ah, bh, biash, epi=O.EPI_RELU, interp=True)
+    ok, ma, mr, w = O.compare(got, want_interp, 0.0)
+    assert ok, f"not bit-exact vs interpreter: max_abs {ma} at {w}"
+    want_ref = O.matmul(ah, bh, biash, epi=O.EPI_RELU, interp=False)
+    check(got, want_ref, 1e-4, "fp32 vs double oracle")
+
+
+def test_fp32_ragged(cuda):
+    a, ah = seeded((37, 53), "a", 9, dtype=torch.float32)
+    b, bh = seeded((53, 29), "b", 9, dtype=torch.float32)
+    c = ops.gemm(a, b)
+    assert np.array_equal(to_host(c), O.matmul(ah, bh, interp=True))
+
+
+def test_batched_matmul(cuda):
+    a, ah = seeded((2, 2, 3, 4), "x", 32, dtype=torch.float32)
+    b, bh = seeded((2, 2, 4, 5), "y", 32, dtype=torch.float32)
+    c = ops.gemm_batched(a, b)
+    check(to_host(c), O.batch_matmul(ah, bh), 1e-6, "batch_matmul")
+
+
+def test_unaligned_bf16_runs_simt_path(cuda):
+    # K = 20 -> row pitch 40 B, not TMA-addressable: SIMT kernel, same contract
+    run_case(cuda, 33, 40, 20, out=torch.float32, epi=Epilogue.BIAS_RELU)
