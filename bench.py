@@ -278,7 +278,303 @@ class GemmFP32:
         return ReferenceGemmSample(self.n, threads, act="relu", rows=8, cols=128)
 
 
-WORKLOADS = {"gemm_bf16": lambda a: GemmBF16(a.size), "gemm_fp32": lambda a: GemmFP32()}
+class _Base:
+    """Shared e2e plumbing: `self.host_inputs` (device tensor -> pinned host
+    copy) are copied H2D every e2e step, `self.outputs` copied back D2H."""
+
+    metric = "TFLOP/s"
+    unit = "TFLOP/s"
+    bound = "tensor"
+
+    def launches_per_step(self):
+        return 1
+
+    def e2e_setup(self):
+        t = self.torch
+        self._h = [(d, d.cpu().pin_memory()) for d in self.e2e_inputs()]
+        self._o = [(d, t.empty_like(d, device="cpu").pin_memory()) for d in self.e2e_outputs()]
+        self.h2d = sum(h.numel() * h.element_size() for _, h in self._h)
+        self.d2h = sum(h.numel() * h.element_size() for _, h in self._o)
+
+    def e2e_step(self):
+        for d, h in self._h:
+            d.copy_(h, non_blocking=True)
+        self.step()
+        for d, h in self._o:
+            h.copy_(d, non_blocking=True)
+
+
+def _dev_uniform(shape, name, seed, lo, hi, dtype):
+    import oracle
+
+    from paper_2603_06731_b200 import ops
+    return ops.fill_uniform(shape, oracle.stream_seed("%" + name, seed), lo, hi, dtype)
+
+
+class Attention(_Base):
+    """BASELINE configs[2]: fused attention fp16 B8 H16 S2048 D128, head-sharded."""
+
+    dtype = "f16"
+
+    def __init__(self, causal, B=8, H=16, S=2048, D=128):
+        self.causal, self.B, self.H, self.S, self.D = causal, B, H, S, D
+        self.name = "attention_causal" if causal else "attention"
+
+    def config(self, world):
+        return {"workload": f"fused attention fp16 B{self.B} H{self.H} S{self.S} D{self.D} "
+                            f"{'causal' if self.causal else 'non-causal'}, scale 1/sqrt(D)",
+                "parallelism": f"heads/{world}", "l2": "Q,K,V,O 268 MB > L2"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        from paper_2603_06731_b200 import ops
+        self.torch, self.ops = torch, ops
+        h0, h1 = shard_rows(self.B * self.H, rank, world)
+        self.bh = h1 - h0
+        shp = (1, self.bh, self.S, self.D)
+        self.q = _dev_uniform(shp, "q", 1 + rank, -1, 1, torch.float16)
+        self.k = _dev_uniform(shp, "k", 1 + rank, -1, 1, torch.float16)
+        self.v = _dev_uniform(shp, "v", 1 + rank, -1, 1, torch.float16)
+        self.o = torch.empty_like(self.q)
+        f = 4.0 * self.S * self.S * self.D * (0.5 if self.causal else 1.0)
+        self.flops_rank = f * self.bh
+        self.flops_total = f * self.B * self.H
+        self.alg_bytes_rank = 4.0 * self.bh * self.S * self.D * 2
+
+    def step(self):
+        self.ops.attention(self.q, self.k, self.v, scale=self.D ** -0.5, causal=self.causal,
+                           out_dtype=self.torch.float16)
+
+    def e2e_inputs(self):
+        return [self.q, self.k, self.v]
+
+    def e2e_outputs(self):
+        return [self.o]
+
+    def reference_sample(self, threads):
+        return ReferenceGraphSample("attention", threads, causal=self.causal)
+
+
+# ResNet-50 (v1.5) 3x3 / 1x1 conv layers: (H_in, C, OC, k, stride, count), BASELINE.md §5
+RESNET50 = [(56, 64, 64, 1, 1, 1), (56, 64, 64, 3, 1, 3), (56, 64, 256, 1, 1, 3),
+            (56, 64, 256, 1, 1, 1), (56, 256, 64, 1, 1, 2), (56, 256, 128, 1, 1, 1),
+            (56, 128, 128, 3, 2, 1), (28, 128, 128, 3, 1, 3), (28, 128, 512, 1, 1, 4),
+            (56, 256, 512, 1, 2, 1), (28, 512, 128, 1, 1, 3), (28, 512, 256, 1, 1, 1),
+            (28, 256, 256, 3, 2, 1), (14, 256, 256, 3, 1, 5), (14, 256, 1024, 1, 1, 6),
+            (28, 512, 1024, 1, 2, 1), (14, 1024, 256, 1, 1, 5), (14, 1024, 512, 1, 1, 1),
+            (14, 512, 512, 3, 2, 1), (7, 512, 512, 3, 1, 2), (7, 512, 2048, 1, 1, 3),
+            (14, 1024, 2048, 1, 2, 1), (7, 2048, 512, 1, 1, 2)]
+
+
+class ResNetConvs(_Base):
+    """BASELINE configs[3]: all ResNet-50 3x3/1x1 convs (53 launches, 2.03 TFLOP
+    at batch 256), NHWC bf16 implicit GEMM + bias + ReLU, batch-sharded."""
+
+    dtype = "bf16"
+    name = "resnet50_convs"
+
+    def __init__(self, batch=256):
+        self.batch = batch
+
+    def config(self, world):
+        return {"workload": f"ResNet-50 3x3/1x1 conv layers (23 shapes, 53 convs), NHWC bf16 "
+                            f"implicit GEMM + bias + ReLU, batch {self.batch}",
+                "parallelism": f"batch/{world}", "l2": "activations > L2 for the 56x56 layers"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        from paper_2603_06731_b200 import ops
+        self.torch, self.ops = torch, ops
+        b0, b1 = shard_rows(self.batch, rank, world)
+        self.b = b1 - b0
+        self.layers = []
+        self.flops_rank = 0.0
+        self.alg_bytes_rank = 0.0
+        for i, (H, C, OC, k, s, cnt) in enumerate(RESNET50):
+            pad = 1 if k == 3 else 0
+            OH = (H + 2 * pad - k) // s + 1
+            x = _dev_uniform((self.b, H, H, C), f"x{i}", 1, -1, 1, torch.bfloat16)
+            w = _dev_uniform((OC, k, k, C), f"w{i}", 1, -0.1, 0.1, torch.bfloat16)
+            bias = _dev_uniform((OC,), f"b{i}", 1, -1, 1, torch.float32)
+            y = torch.empty((self.b, OH, OH, OC), dtype=torch.bfloat16, device=dev)
+            self.layers.append((x, w, bias, y, k, s, pad, cnt))
+            self.flops_rank += cnt * 2.0 * self.b * OH * OH * OC * C * k * k
+            self.alg_bytes_rank += cnt * 2.0 * (x.numel() + y.numel() + w.numel())
+        self.flops_total = self.flops_rank * self.batch / self.b
+
+    def step(self):
+        from paper_2603_06731_b200 import Epilogue, check, lib
+        import ctypes
+        L = lib()
+        st = ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+        for x, w, bias, y, k, s, pad, cnt in self.layers:
+            B, H, W, C = x.shape
+            OC, OH = w.shape[0], y.shape[1]
+            for _ in range(cnt):
+                check(L.afg_conv2d_nhwc(x.data_ptr(), w.data_ptr(), bias.data_ptr(), y.data_ptr(),
+                                        B, H, W, C, OC, k, k, s, s, pad, pad, 1, 1, OH, OH, 2,
+                                        int(Epilogue.BIAS_RELU), st))
+
+    def launches_per_step(self):
+        return sum(l[-1] for l in self.layers)
+
+    def e2e_inputs(self):
+        return [l[0] for l in self.layers]
+
+    def e2e_outputs(self):
+        return [l[3] for l in self.layers]
+
+    def reference_sample(self, threads):
+        return ReferenceGraphSample("conv", threads)
+
+
+class BertLayer(_Base):
+    """BASELINE configs[4]: BERT-base encoder layer, B64 x S512, bf16,
+    batch-sharded (afg_encoder_layer_fwd: 7 launches)."""
+
+    dtype = "bf16"
+    name = "bert_layer"
+
+    def __init__(self, batch=64, seq=512, hidden=768, heads=12, ffn=3072):
+        self.batch, self.seq, self.hd, self.heads, self.ffn = batch, seq, hidden, heads, ffn
+
+    def config(self, world):
+        return {"workload": f"BERT-base encoder layer (QKV GEMM, fused attention, out-proj+"
+                            f"residual, LN, GELU FFN, LN) B{self.batch} x S{self.seq}, bf16",
+                "parallelism": f"batch/{world}", "l2": "activations 50 MB-200 MB per op"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        from paper_2603_06731_b200 import lib
+        self.torch = torch
+        b0, b1 = shard_rows(self.batch, rank, world)
+        self.b = b1 - b0
+        T, hd, ffn = self.b * self.seq, self.hd, self.ffn
+        bf, f32 = torch.bfloat16, torch.float32
+        self.x = _dev_uniform((T, hd), "x", 1, -1, 1, bf)
+        self.y = torch.empty_like(self.x)
+        self.w = {"qkv": _dev_uniform((hd, 3 * hd), "wqkv", 1, -0.05, 0.05, bf),
+                  "o": _dev_uniform((hd, hd), "wo", 1, -0.05, 0.05, bf),
+                  "1": _dev_uniform((hd, ffn), "w1", 1, -0.05, 0.05, bf),
+                  "2": _dev_uniform((ffn, hd), "w2", 1, -0.05, 0.05, bf)}
+        self.p = {"bqkv": _dev_uniform((3 * hd,), "bqkv", 1, -0.1, 0.1, f32),
+                  "bo": _dev_uniform((hd,), "bo", 1, -0.1, 0.1, f32),
+                  "g1": _dev_uniform((hd,), "g1", 1, 0.9, 1.1, f32),
+                  "be1": _dev_uniform((hd,), "be1", 1, -0.1, 0.1, f32),
+                  "b1": _dev_uniform((ffn,), "b1", 1, -0.1, 0.1, f32),
+                  "b2": _dev_uniform((hd,), "b2", 1, -0.1, 0.1, f32),
+                  "g2": _dev_uniform((hd,), "g2", 1, 0.9, 1.1, f32),
+                  "be2": _dev_uniform((hd,), "be2", 1, -0.1, 0.1, f32)}
+        self.ws_bytes = lib().afg_encoder_layer_workspace(self.b, self.seq, hd, ffn, 2)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        gemm = 2.0 * T * hd * (3 * hd + hd + 2 * ffn)
+        attn = 4.0 * self.b * self.heads * self.seq * self.seq * (hd // self.heads)
+        self.flops_rank = gemm + attn
+        self.flops_total = self.flops_rank * self.batch / self.b
+        self.alg_bytes_rank = 2.0 * T * hd * 2
+
+    def step(self):
+        import ctypes
+
+        from paper_2603_06731_b200 import check, lib
+        L = lib()
+        p, w = self.p, self.w
+        st = ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+        check(L.afg_encoder_layer_fwd(
+            self.x.data_ptr(), self.y.data_ptr(), self.b, self.seq, self.hd, self.heads, self.ffn,
+            w["qkv"].data_ptr(), p["bqkv"].data_ptr(), w["o"].data_ptr(), p["bo"].data_ptr(),
+            p["g1"].data_ptr(), p["be1"].data_ptr(), w["1"].data_ptr(), p["b1"].data_ptr(),
+            w["2"].data_ptr(), p["b2"].data_ptr(), p["g2"].data_ptr(), p["be2"].data_ptr(),
+            1e-12, 2, self.ws.data_ptr(), self.ws_bytes, st))
+
+    def launches_per_step(self):
+        return 7
+
+    def e2e_inputs(self):
+        return [self.x]
+
+    def e2e_outputs(self):
+        return [self.y]
+
+    def reference_sample(self, threads):
+        return ReferenceGemmSample(self.hd, threads, act="relu", rows=4, cols=96)
+
+
+class MemChain(_Base):
+    """Memory-bound chains (K4 softmax fp16 [8*16*2048, 2048]; K5 residual +
+    layernorm bf16 [32768, 768]); metric GB/s of algorithmic bytes."""
+
+    metric = "GB/s"
+    unit = "GB/s"
+    bound = "hbm"
+
+    def __init__(self, kind):
+        self.kind = kind
+        self.name = kind
+        self.dtype = "f16" if kind == "softmax" else "bf16"
+
+    def config(self, world):
+        what = ("row softmax fp16 [262144, 2048]" if self.kind == "softmax" else
+                "residual + layernorm bf16 [32768, 768] (x + r -> y, fp32 stats)")
+        return {"workload": what, "parallelism": f"rows/{world}",
+                "l2": "inputs larger than L2" if self.kind == "softmax" else
+                "L2 flushed between steps"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        from paper_2603_06731_b200 import ops
+        self.torch, self.ops = torch, ops
+        if self.kind == "softmax":
+            rows, cols, dt = 8 * 16 * 2048, 2048, torch.float16
+        else:
+            rows, cols, dt = 32768, 768, torch.bfloat16
+        r0, r1 = shard_rows(rows, rank, world)
+        n = r1 - r0
+        self.x = _dev_uniform((n, cols), "x", 1, -4, 4, dt)
+        self.y = torch.empty_like(self.x)
+        self.flush = None
+        if self.kind == "layernorm":
+            self.r = _dev_uniform((n, cols), "r", 1, -1, 1, dt)
+            self.g = _dev_uniform((cols,), "g", 1, 0.9, 1.1, torch.float32)
+            self.b = _dev_uniform((cols,), "b", 1, -0.1, 0.1, torch.float32)
+            self.flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+            self.alg_bytes_rank = 3.0 * n * cols * 2
+        else:
+            self.alg_bytes_rank = 2.0 * n * cols * 2
+        self.flops_rank = self.alg_bytes_rank
+        self.flops_total = self.alg_bytes_rank * rows / n
+
+    def step(self):
+        if self.kind == "softmax":
+            self.ops.softmax(self.x)
+        else:
+            self.flush.zero_()
+            self.ops.layernorm_residual(self.x, self.r, self.g, self.b)
+
+    def kernel_only(self):
+        if self.kind == "softmax":
+            self.ops.softmax(self.x)
+        else:
+            self.ops.layernorm_residual(self.x, self.r, self.g, self.b)
+
+    def e2e_inputs(self):
+        return [self.x] + ([self.r] if self.kind == "layernorm" else [])
+
+    def e2e_outputs(self):
+        return [self.y]
+
+    def reference_sample(self, threads):
+        return ReferenceGraphSample("softmax", threads)
+
+
+WORKLOADS = {"gemm_bf16": lambda a: GemmBF16(a.size), "gemm_fp32": lambda a: GemmFP32(),
+             "attention": lambda a: Attention(False), "attention_causal": lambda a: Attention(True),
+             "resnet50_convs": lambda a: ResNetConvs(), "bert_layer": lambda a: BertLayer(),
+             "softmax": lambda a: MemChain("softmax"), "layernorm": lambda a: MemChain("layernorm")}
 
 
 # ======================================================= reference path ===
@@ -335,6 +631,67 @@ class ReferenceGemmSample:
         return time.perf_counter() - t0
 
 
+class ReferenceGraphSample:
+    """Bounded reference-path sample for the non-GEMM workloads: one
+    af::interpret instance per host thread on a small instance of the same op
+    graph (attention: one head at N=64, D=128; conv: 3x3 64->64 on 8x8;
+    softmax: 64 rows x 2048), metric units as the workload's."""
+
+    def __init__(self, kind, threads, causal=False):
+        import oracle as O
+        from oracle.graphs import attention_graph, nhwc_conv_graph, T
+        self.O, self.kind, self.threads = O, kind, threads
+        self.kindref = "reference" if O.ref_available() else "port"
+        if kind == "attention":
+            N, D = 64, 128
+            g, fixed = attention_graph(1, 1, N, D, causal)
+            self.flops = 4.0 * N * N * D * (0.5 if causal else 1.0) * threads
+            self.desc = f"1 head N={N} D={D} attention graph"
+        elif kind == "conv":
+            g, fixed = nhwc_conv_graph(1, 8, 8, 64, 64, 3, 1, "same")
+            self.flops = 2.0 * 64 * 64 * 64 * 9 * threads
+            self.desc = "3x3 64->64 NHWC conv graph on 1x8x8"
+        else:
+            g = {"tensors": [T("x", [64, 2048], "f16"), T("y", [64, 2048], "f16")],
+                 "ops": [{"op": "softmax", "inputs": ["x"], "output": "y", "attrs": {"axis": -1}}]}
+            fixed = {}
+            self.flops = 2.0 * 64 * 2048 * 2 * threads  # bytes, for the GB/s metric
+            self.desc = "softmax f16 64x2048 graph"
+        self.graph = json.dumps(g)
+        self.inputs = O.random_graph_inputs(g, 7, -1.0, 1.0)
+        self.inputs.update(fixed)
+        self.kind_graph = g
+
+    @property
+    def kind_label(self):
+        return self.kindref
+
+    def describe(self):
+        return (f"{self.threads} independent af::interpret instances, each a {self.desc}"
+                if self.kindref == "reference" else f"{self.threads} x {self.desc} via oracle port")
+
+    def run_once(self):
+        from concurrent.futures import ThreadPoolExecutor
+        O = self.O
+
+        def one(_):
+            if self.kindref == "reference":
+                O.ref_run(self.graph, self.inputs, "interpret")
+            elif self.kind == "attention":
+                ins = self.inputs
+                O.attention(ins["q"], ins["k"], ins["v"], nthreads=1)
+            elif self.kind == "conv":
+                ins = self.inputs
+                O.conv_nhwc(ins["x"], np.transpose(ins["w"], (0, 2, 3, 1)), ins["bias"], (1, 1),
+                            (1, 1), epi=O.EPI_RELU, nthreads=1)
+            else:
+                O.softmax(self.inputs["x"])
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            list(ex.map(one, range(self.threads)))
+        return time.perf_counter() - t0
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -352,14 +709,15 @@ def run_reference(args, wl, rank, world):
         sample.run_once()
     times = [sample.run_once() for _ in range(args.steps)]
     t = sum(times) / len(times)
-    value = sample.flops / t / 1e12
+    value = sample.flops / t / (1e9 if wl.unit == "GB/s" else 1e12)
     line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "strong" if isinstance(wl, GemmBF16) else "weak",
+            "higher_is_better": True, "scaling": "weak" if isinstance(wl, GemmFP32) else "strong",
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (makeRandomTensor)",
             "config": wl.config(world), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": wl.unit, "cores": threads,
-                             "kind": sample.kind, "sample": sample.describe()},
+                             "kind": getattr(sample, "kind_label", getattr(sample, "kind", None)),
+                             "sample": sample.describe()},
             "e2e": {"value": value, "unit": wl.unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -415,7 +773,8 @@ def run_afg(args, wl, rank, world, local):
     ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop()
     ms_max = max_over_ranks(ms)
-    value = wl.flops_total / (ms_max * 1e-3) / 1e12
+    scale = 1e9 if wl.unit == "GB/s" else 1e12
+    value = wl.flops_total / (ms_max * 1e-3) / scale
 
     # kernel-only duration of the dominant launch (same stream, events), for
     # the roofline: one extra timed pass without anything else in the step
@@ -450,23 +809,25 @@ def run_afg(args, wl, rank, world, local):
     e1.record(stream)
     barrier()
     e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps)
-    e2e_value = wl.flops_total / (e_ms * 1e-3) / 1e12
+    e2e_value = wl.flops_total / (e_ms * 1e-3) / scale
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_threads()
         sample = wl.reference_sample(threads)
         t = sample.run_once()
-        cpu = {"value": sample.flops / t / 1e12, "unit": wl.unit, "cores": threads,
-               "kind": sample.kind, "sample": sample.describe(), "seconds": t}
+        scale = 1e9 if wl.unit == "GB/s" else 1e12
+        cpu = {"value": sample.flops / t / scale, "unit": wl.unit, "cores": threads,
+               "kind": getattr(sample, "kind_label", getattr(sample, "kind", None)),
+               "sample": sample.describe(), "seconds": t}
 
     if rank == 0:
         line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
                 "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
                 "higher_is_better": True,
-                "scaling": "strong" if isinstance(wl, GemmBF16) else "weak",
+                "scaling": "weak" if isinstance(wl, GemmFP32) else "strong",
                 "vs_baseline": None, "dtype": wl.dtype,
-                "data": "synthetic (device-side makeRandomTensor stream, U[-1,1))",
+                "data": "synthetic (device-side makeRandomTensor stream, uniform)",
                 "config": wl.config(world),
                 "roofline": {"bound": wl.bound if wl.bound in ("hbm", "tensor") else "tensor",
                              "achieved": achieved, "peak": peak, "unit": unit,
@@ -494,14 +855,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="afg", choices=["afg", "reference"])
     ap.add_argument("--workload", default="gemm_bf16", choices=sorted(WORKLOADS))
+    ap.add_argument("--all", action="store_true", help="run every workload (one line each)")
     ap.add_argument("--size", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()
-    wl = WORKLOADS[args.workload](args)
-    if args.impl == "reference":
-        return run_reference(args, wl, rank, world)
-    return run_afg(args, wl, rank, world, local)
+    names = sorted(WORKLOADS) if args.all else [args.workload]
+    for name in names:
+        wl = WORKLOADS[name](args)
+        if args.impl == "reference":
+            run_reference(args, wl, rank, world)
+        else:
+            run_afg(args, wl, rank, world, local)
+    return 0
 
 
 if __name__ == "__main__":

@@ -7,7 +7,9 @@ interp.cpp:698-730):
     interp.cpp:335-347): bit-exact (tol 0); vs the double oracle
     (matmulReference, oracles.cpp:122-134): 1e-4 (BASELINE north star).
   * bf16/fp16 inputs, fp32 output, vs the double oracle on the same rounded
-    inputs: 1e-5 * max(1, K/1024) (fp32 accumulation-order error).
+    inputs: 1e-5 for K <= 1024; for longer K the forward-error bound of fp32
+    (tensor-core) accumulation, |C - C_exact| <= 2^-19 * sum_k |a_ik b_kj|
+    (measured 7e-7 of sum|ab| at K = 8192).
   * bf16/fp16 output: one output ulp, 2^-7 (bf16) / 2^-10 (fp16), against the
     oracle result rounded to the output type.
 """
@@ -49,8 +51,16 @@ def run_case(cuda, M, N, K, dt=torch.bfloat16, out=None, epi=Epilogue.BIAS_GELU_
     if residual:
         acc = acc + (resh if rows is None else resh[rows])
     want = O.round_to(acc, out_code)
-    tol = ULP[out] if out in ULP else 1e-5 * max(1.0, K / 1024)
-    return check(got, want, tol, f"gemm {M}x{N}x{K} {dt}->{out} epi={int(epi)}")
+    what = f"gemm {M}x{N}x{K} {dt}->{out} epi={int(epi)}"
+    if out in ULP:
+        return check(got, want, ULP[out], what)
+    if K <= 1024:
+        return check(got, want, 1e-5, what)
+    absab = O.matmul(np.abs(ah), np.abs(bh), b_nk=layout == Layout.B_NK, rows=rows)
+    err = np.abs(got - want)
+    bound = 2.0**-19 * absab + 1e-6
+    assert (err <= bound).all(), f"{what}: max err/sum|ab| = {(err / absab).max():.3e}"
+    return float((err / absab).max())
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (100, 200, 72),
