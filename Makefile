@@ -12,7 +12,7 @@ CU_SRCS   := $(wildcard $(SRC_DIR)/*.cu)
 CPP_SRCS  := $(wildcard $(SRC_DIR)/*.cpp)
 OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) \
              $(patsubst $(SRC_DIR)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS))
-HDRS      := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.h) include/afg.h
+HDRS      := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.h) $(wildcard include/*.h)
 LIB       := $(PKG)/libafg.so
 
 .PHONY: all lib oracle clean sass

@@ -22,6 +22,10 @@
 #include <string>
 #include <vector>
 
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)  // exported from libafg.so (built -fvisibility=hidden)
+#endif
+
 namespace afg {
 namespace gpu {
 
@@ -102,3 +106,7 @@ std::map<std::string, TensorValue> execute(const TensorGraph& g,
 
 }  // namespace gpu
 }  // namespace afg
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif

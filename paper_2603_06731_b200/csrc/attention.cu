@@ -37,7 +37,6 @@ using namespace sm100;
 
 constexpr int BM = 128;  // query rows per CTA
 constexpr int BN = 128;  // keys per KV tile
-constexpr int KV_STAGES = 2;
 
 struct AttnArgs {
   const float* bias;  // [BH, Nq, Nk] or null
@@ -51,16 +50,15 @@ struct AttnArgs {
 
 template <int D>
 struct AttnSmem {
-  static constexpr int TILE = BM * D * 2;  // Q / K / V tile bytes (BM == BN)
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + TILE;
+  static constexpr int KV_STAGES = D == 64 ? 4 : 2;
+  static constexpr int TILE = BM * D * 2;  // one Q / K / V tile (BM == BN rows)
+  static constexpr int QA_OFF = 0;
+  static constexpr int QB_OFF = TILE;
+  static constexpr int K_OFF = 2 * TILE;
   static constexpr int V_OFF = K_OFF + KV_STAGES * TILE;
-  static constexpr int P_OFF = V_OFF + KV_STAGES * TILE;
-  static constexpr int P_BYTES = BM * BN * 2;
-  static constexpr int BAR_OFF = P_OFF + P_BYTES;
-  // bars: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2],
-  //       p_full, pv_done
-  static constexpr int NUM_BARS = 1 + 4 * KV_STAGES + 4 + 2;
+  static constexpr int BAR_OFF = V_OFF + KV_STAGES * TILE;
+  // q_full, k_full[S], k_empty[S], v_full[S], v_empty[S], s_full[2], p_full[2], o_done
+  static constexpr int NUM_BARS = 1 + 4 * KV_STAGES + 5;
   static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
 };
 
@@ -74,15 +72,22 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf16) {
   return bf16 ? pack_bf16(a, b) : pack_f16(a, b);
 }
 
+// One CTA = one (b, h) x two 128-row query tiles A and B ("ping-pong"): while
+// the softmax warpgroup of one tile works, the tensor core runs the other
+// tile's MMAs. TMEM (512 columns): S_A [0,128) S_B [128,256) O_A, O_B after.
+// P is written back over S as packed 16-bit values and consumed by the PV MMA
+// straight from TMEM (A operand in tensor memory), so shared memory holds only
+// Q_A, Q_B and the K / V ring.
+// Warps: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4-7 softmax A, 8-11 softmax B.
 template <int D, bool BF16>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnArgs args) {
   using L = AttnSmem<D>;
-  constexpr int DB = D / 64;  // 128-byte swizzle atoms per row of Q/K/V
+  constexpr int KS = L::KV_STAGES;
+  constexpr int DB = D / 64;  // 128-byte swizzle atoms per row
   constexpr uint32_t TMEM_COLS = 512;
-  constexpr uint32_t O_COL = 2 * BN;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -90,45 +95,52 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + KV_STAGES;
-  uint64_t* v_full = k_empty + KV_STAGES;
-  uint64_t* v_empty = v_full + KV_STAGES;
-  uint64_t* s_full = v_empty + KV_STAGES;
-  uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;
-  uint64_t* pv_done = p_full + 1;
+  uint64_t* k_empty = k_full + KS;
+  uint64_t* v_full = k_empty + KS;
+  uint64_t* v_empty = v_full + KS;
+  uint64_t* s_full = v_empty + KS;  // [2]
+  uint64_t* p_full = s_full + 2;    // [2]
+  uint64_t* o_done = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
 
-  // heavy causal tiles first: reverse the q-tile order
-  const int n_qtiles = (args.Nq + BM - 1) / BM;
-  const int qt = n_qtiles - 1 - static_cast<int>(blockIdx.x);
+  const int n_pairs = (args.Nq + 2 * BM - 1) / (2 * BM);
+  const int qp = n_pairs - 1 - static_cast<int>(blockIdx.x);  // heavy causal pairs first
   const int bh = blockIdx.y;
   const int hh = bh % args.H;
   const int bb = bh / args.H;
-  const int q0 = qt * BM;
-  int n_kv = (args.Nk + BN - 1) / BN;
-  if (args.causal) n_kv = min(n_kv, (q0 + BM - 1) / BN + 1);
+  const int q0 = qp * 2 * BM;
+  const int nkv_all = (args.Nk + BN - 1) / BN;
+  int nkv[2];
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int first = q0 + g * BM;
+    if (first >= args.Nq) {
+      nkv[g] = 0;
+    } else {
+      nkv[g] = args.causal ? min(nkv_all, (first + BM - 1) / BN + 1) : nkv_all;
+    }
+  }
+  const int nkv_max = max(nkv[0], nkv[1]);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < KV_STAGES; ++s) {
+    for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], 128);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1);
+      mbar_init(&p_full[g], 128);
     }
-    mbar_init(p_full, 128);
-    mbar_init(pv_done, 1);
+    mbar_init(o_done, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -136,16 +148,20 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t S_COL[2] = {0u, static_cast<uint32_t>(BN)};
+  const uint32_t O_COL[2] = {static_cast<uint32_t>(2 * BN), static_cast<uint32_t>(2 * BN + D)};
 
   if (warp == 0) {
     // --------------------------------------------------------------- TMA --
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, L::TILE);
-      for (int a = 0; a < DB; ++a)
-        tma_load_4d(smem + L::Q_OFF + a * (BM * 128), &tmQ, q_full, a * 64, q0, hh, bb);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % KV_STAGES;
-        const uint32_t ph = (j / KV_STAGES) & 1;
+      mbar_arrive_expect_tx(q_full, 2 * L::TILE);
+      for (int g = 0; g < 2; ++g)
+        for (int a = 0; a < DB; ++a)
+          tma_load_4d(smem + (g ? L::QB_OFF : L::QA_OFF) + a * (BM * 128), &tmQ, q_full, a * 64,
+                      q0 + g * BM, hh, bb);
+      for (int j = 0; j < nkv_max; ++j) {
+        const int st = j % KS;
+        const uint32_t ph = (j / KS) & 1;
         mbar_wait(&k_empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&k_full[st], L::TILE);
         for (int a = 0; a < DB; ++a)
@@ -163,145 +179,168 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_f16(BM, BN, BF16 ? 1u : 0u, 0u, 0u);
       constexpr uint32_t idesc_o = idesc_f16(BM, D, BF16 ? 1u : 0u, 0u, 1u);
-      const uint32_t q_addr = smem_u32(smem + L::Q_OFF);
-      const uint32_t p_addr = smem_u32(smem + L::P_OFF);
-      auto issue_s = [&](int j) {
-        const int st = j % KV_STAGES;
-        const int sb = j & 1;
-        if (j >= 2) mbar_wait(&s_free[sb], ((j - 2) >> 1) & 1);
-        mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(smem + L::K_OFF + st * L::TILE);
+      const uint32_t q_addr[2] = {smem_u32(smem + L::QA_OFF), smem_u32(smem + L::QB_OFF)};
+      auto issue_s = [&](int g, int j) {
+        const uint32_t k_addr = smem_u32(smem + L::K_OFF + (j % KS) * L::TILE);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk / 4) * (BM * 128) + (kk % 4) * 32;
-          mma_f16_ss(tmem + sb * BN, desc_kmajor_sw128(q_addr + off),
-                     desc_kmajor_sw128(k_addr + (kk / 4) * (BN * 128) + (kk % 4) * 32), idesc_s,
-                     kk > 0 ? 1u : 0u);
+          mma_f16_ss(tmem + S_COL[g], desc_kmajor_sw128(q_addr[g] + off),
+                     desc_kmajor_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&s_full[sb]);
-        mma_commit(&k_empty[st]);
+        mma_commit(&s_full[g]);
+      };
+      auto issue_pv = [&](int g, int j) {
+        const uint32_t v_addr = smem_u32(smem + L::V_OFF + (j % KS) * L::TILE);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_f16_ts(tmem + O_COL[g], tmem + S_COL[g] + kk * 8,
+                     desc_mnmajor_sw128(v_addr + kk * 16 * 128, BN * 128), idesc_o,
+                     (j > 0 || kk > 0) ? 1u : 0u);
       };
       mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
       tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < n_kv; ++j) {
-        if (j + 1 < n_kv) issue_s(j + 1);
-        const int st = j % KV_STAGES;
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(smem + L::V_OFF + st * L::TILE);
+      if (nkv[0] > 0) issue_s(0, 0);
+      if (nkv[1] > 0) issue_s(1, 0);
+      mma_commit(&k_empty[0]);
+      for (int j = 0; j < nkv_max; ++j) {
+        const int st = j % KS;
+        const int jn = j + 1;
+        bool k_next_ready = false;
+        mbar_wait(&v_full[st], (j / KS) & 1);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t a = desc_kmajor_sw128(p_addr + (kk / 4) * (BM * 128) + (kk % 4) * 32);
-          const uint64_t b = desc_mnmajor_sw128(v_addr + kk * 16 * 128, BN * 128);
-          mma_f16_ss(tmem + O_COL, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int g = 0; g < 2; ++g) {
+          if (j < nkv[g]) {
+            mbar_wait(&p_full[g], j & 1);
+            tc_fence_after();
+            issue_pv(g, j);
+            if (jn < nkv[g]) {
+              if (!k_next_ready) {
+                mbar_wait(&k_full[jn % KS], (jn / KS) & 1);
+                tc_fence_after();
+                k_next_ready = true;
+              }
+              issue_s(g, jn);  // runs after PV(g, j) on the tensor pipe: P(j) consumed first
+            }
+          }
         }
-        mma_commit(pv_done);
         mma_commit(&v_empty[st]);
+        if (k_next_ready) mma_commit(&k_empty[jn % KS]);
       }
+      mma_commit(o_done);
     }
   } else if (warp >= 4) {
-    // ------------------------------------------ softmax / correction / out --
-    const int w4 = warp - 4;
-    const int row = w4 * 32 + lane;  // query row within the tile == TMEM lane
-    const int qi = q0 + row;
+    // --------------------------------- softmax / correction / epilogue (per tile)
+    const int g = (warp - 4) / 4;
+    const int w4 = warp % 4;
+    const int row = w4 * 32 + lane;
+    const int qi = q0 + g * BM + row;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
-    const uint32_t p_row = smem_u32(smem + L::P_OFF) + row * 128;
+    const uint32_t s_base = lane_base + S_COL[g];
+    const uint32_t o_base = lane_base + O_COL[g];
     const float* brow =
         args.bias ? args.bias + (static_cast<int64_t>(bh) * args.Nq + min(qi, args.Nq - 1)) *
                                     args.Nk
                   : nullptr;
-    float m = -INFINITY;  // running max, in scaled log2 units
+    float m = -INFINITY;  // running max (scaled log2 units)
     float l = 0.0f;
-    for (int j = 0; j < n_kv; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+    for (int j = 0; j < nkv[g]; ++j) {
+      mbar_wait(&s_full[g], j & 1);  // also implies PV(g, j-1) completed (in-order MMAs)
       tc_fence_after();
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(lane_base + sb * BN + c * 32, sr[c]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&s_free[sb]);
-      // scale, bias, masks; row max
       const int k0 = j * BN;
+      const bool need_mask = (args.causal && k0 + BN - 1 > q0 + g * BM) || k0 + BN > args.Nk;
+      auto score = [&](uint32_t raw, int kj) {
+        float v = __uint_as_float(raw) * args.scale_log2;
+        if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
+        if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
+        return v;
+      };
+      // Fast path (no additive bias, no mask in this tile, scale > 0): the max
+      // is taken on the raw scores and each probability is one FFMA + EX2.
+      // The masked path (causal diagonal / key tail / bias) is per element.
+      const bool fast = brow == nullptr && !need_mask && args.scale_log2 > 0.0f;
       float tmax = -INFINITY;
+      if (fast) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t sr[32];
+          tmem_ld32(s_base + c * 32, sr);
+          tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+          for (int e = 0; e < 32; e += 2)
+            tmax = fmaxf(tmax, fmaxf(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])));
+        }
+        tmax *= args.scale_log2;
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t sr[32];
+          tmem_ld32(s_base + c * 32, sr);
+          tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int kj = k0 + c * 32 + e;
-          float v = __uint_as_float(sr[c][e]) * args.scale_log2;
-          if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
-          if (kj >= args.Nk || (args.causal && kj > qi)) v = -INFINITY;
-          sr[c][e] = __float_as_uint(v);
-          tmax = fmaxf(tmax, v);
+          for (int e = 0; e < 32; ++e) tmax = fmaxf(tmax, score(sr[e], k0 + c * 32 + e));
         }
       }
       const float m_new = fmaxf(m, tmax);
       const float base = m_new == -INFINITY ? 0.0f : m_new;
-      const float alpha = ex2(m - base);  // 0 on the first tile (m = -inf)
-      float tsum = 0.0f;
-      uint32_t pk[4][16];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float p0 = ex2(__uint_as_float(sr[c][2 * e]) - base);
-          const float p1 = ex2(__uint_as_float(sr[c][2 * e + 1]) - base);
-          tsum += p0 + p1;
-          pk[c][e] = pack2(p0, p1, BF16);
-        }
-      }
-      l = l * alpha + tsum;
-      // P buffer and O are owned by the PV MMA of the previous tile
-      if (j > 0) {
-        mbar_wait(pv_done, (j - 1) & 1);
-        tc_fence_after();
-        // correction O *= exp(m_old - m_new), once per tile. tcgen05.ld/st are
-        // warp-collective: the decision must be warp-uniform (rows whose max
-        // did not move scale by alpha == 1).
-        if (__any_sync(0xffffffffu, m_new > m)) {
+      const float alpha = ex2(m - base);  // 0 on the first tile
+      // correction O *= exp(m_old - m_new) once per tile (warp-uniform decision:
+      // tcgen05.ld/st are warp-collective; rows whose max did not move use 1)
+      if (j > 0 && __any_sync(0xffffffffu, m_new > m)) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(lane_base + O_COL + c * 32, o);
-            tmem_wait_ld();
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(o_base + c * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(lane_base + O_COL + c * 32, o);
-          }
-          tmem_wait_st();
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(o_base + c * 32, o);
         }
       }
       m = m_new;
-      // P (row `row`, 128 keys) -> smem, K-major SWIZZLE_128B, 2 atoms of 64 keys
+      // pass 2: P = exp2(s - m) packed to 16 bit, written over S (cols 16c..)
+      float tsum = 0.0f;
+      const float nb = -base;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t sr[32];
+        tmem_ld32(s_base + c * 32, sr);
+        tmem_wait_ld();
+        uint32_t pk[16];
+        if (fast) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+          for (int e = 0; e < 16; ++e) {
+            const float p0 = ex2(fmaf(__uint_as_float(sr[2 * e]), args.scale_log2, nb));
+            const float p1 = ex2(fmaf(__uint_as_float(sr[2 * e + 1]), args.scale_log2, nb));
+            tsum += p0 + p1;
+            pk[e] = pack2(p0, p1, BF16);
+          }
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int key_chunk = c * 4 + q;  // 16-byte chunk of 8 keys, 0..15
-          const int atom = key_chunk / 8;
-          const int ch = key_chunk % 8;
-          const uint32_t addr = p_row + atom * (BM * 128) + ((ch ^ (row & 7)) * 16);
-          st_shared_v4(addr, pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
+          for (int e = 0; e < 16; ++e) {
+            const float p0 = ex2(score(sr[2 * e], k0 + c * 32 + 2 * e) + nb);
+            const float p1 = ex2(score(sr[2 * e + 1], k0 + c * 32 + 2 * e + 1) + nb);
+            tsum += p0 + p1;
+            pk[e] = pack2(p0, p1, BF16);
+          }
         }
+        tmem_st16(s_base + c * 16, pk);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();
+      l = l * alpha + tsum;
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[g]);
     }
     // ---- epilogue: O / l -> global
-    mbar_wait(pv_done, (n_kv - 1) & 1);
+    mbar_wait(o_done, 0);
     tc_fence_after();
     const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
-    const bool valid = qi < args.Nq;
+    const bool valid = qi < args.Nq && nkv[g] > 0;
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
       uint32_t o[32];
-      tmem_ld32(lane_base + O_COL + c * 32, o);
+      tmem_ld32(o_base + c * 32, o);
       tmem_wait_ld();
       if (!valid) continue;
       const int64_t base_idx = static_cast<int64_t>(bb) * args.o_bs +
@@ -405,8 +444,8 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((a.Nq + BM - 1) / BM, a.BH);
-  kern<<<grid, 256, smem, s>>>(tq, tk, tv, a);
+  dim3 grid((a.Nq + 2 * BM - 1) / (2 * BM), a.BH);
+  kern<<<grid, 384, smem, s>>>(tq, tk, tv, a);
   count_launch();
   return cudaGetLastError();
 }

@@ -122,6 +122,9 @@ def enc(a):
                           if not np.isfinite(v)}}
 
 
+FIXED = {}
+
+
 def main():
     cases = []
     for name, seed, g in FRONTEND:
@@ -134,6 +137,7 @@ def main():
                       "interpret": {k: enc(v) for k, v in interp.items()},
                       "oracle": {k: enc(v) for k, v in orc.items()}})
     for name, seed, g, fixed, lo, hi in PATTERNS:
+        FIXED[name] = fixed
         gj = json.dumps(g)
         inputs = {k[1:]: v for k, v in O.ref_random_inputs(gj, seed, lo, hi).items()}
         inputs.update(fixed)
@@ -144,6 +148,20 @@ def main():
                       "inputs": {k: enc(v) for k, v in inputs.items()},
                       "interpret": {k: enc(v) for k, v in interp.items()},
                       "oracle": {k: enc(v) for k, v in orc.items()}})
+    # the reference-side driver spec (integration/check_lowering_gpu.cpp)
+    spec = []
+    for c in cases:
+        entry = {"name": c["name"], "graph": c["graph"], "seed": c["seed"], "lo": c["lo"],
+                 "hi": c["hi"],
+                 "profile": "Int" if c["name"] == "quant_dequant" else
+                 ("F16Fragment" if "f16" in c["name"] else "F32")}
+        if c.get("fixed"):
+            entry["fixed"] = {k: [("-inf" if v == -np.inf else "inf") if not np.isfinite(v) else v
+                                  for v in np.asarray(FIXED[c["name"]][k]).ravel().tolist()]
+                              for k in c["fixed"]}
+        spec.append(entry)
+    with open(os.path.join(os.path.dirname(__file__), "check_lowering_cases.json"), "w") as f:
+        json.dump({"cases": spec}, f, separators=(",", ":"))
     with open(OUT, "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py",
                    "reference": "/root/reference/proj (AffineForge), built by oracle/Makefile",
