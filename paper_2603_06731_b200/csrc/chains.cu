@@ -13,10 +13,12 @@
 //   elementwise / reduce / convert / transpose / fill: graph-executor tails
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "afg_internal.h"
 #include "epilogue.cuh"
+#include "sm100.cuh"
 
 namespace afg {
 namespace {
@@ -171,7 +173,11 @@ __global__ void __launch_bounds__(256) softmax_block_kernel(const TI* __restrict
 }
 
 template <typename TI, typename TO>
-cudaError_t softmax_launch(const void* x, void* y, int64_t rows, int64_t cols, cudaStream_t s) {
+cudaError_t softmax_launch(const void* x, void* y, int64_t rows, int64_t cols, cudaStream_t s);
+
+template <typename TI, typename TO>
+cudaError_t softmax_launch_direct(const void* x, void* y, int64_t rows, int64_t cols,
+                                  cudaStream_t s) {
   constexpr int E = Vec<TI>::N;
   const bool vec_ok = (cols % E == 0) && (cols % Vec<TO>::N == 0) &&
                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
@@ -196,6 +202,184 @@ cudaError_t softmax_launch(const void* x, void* y, int64_t rows, int64_t cols, c
   }
   count_launch();
   return cudaGetLastError();
+}
+
+// --------------------------------------------------- TMA-streamed chains --
+// Persistent CTA per SM: warp 8 (one lane) streams whole rows global -> smem
+// with 1-D bulk copies into an NS-deep ring (mbarrier complete_tx); warps 0-7
+// each reduce every 8th row out of shared memory and write the result with
+// coalesced 16-byte stores. In-flight bytes live in shared memory (~160 KB
+// per SM), not in registers, so HBM stays saturated.
+constexpr int STREAM_WARPS = 8;
+constexpr int STREAM_SMEM = 160 * 1024;
+
+template <typename TI, typename TO, int MODE, int CH>  // MODE 0 softmax, 1 layernorm
+__global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
+    stream_rows_kernel(const TI* __restrict__ x, const TI* __restrict__ res,
+                       const float* __restrict__ gamma, const float* __restrict__ beta,
+                       TO* __restrict__ y, TO* __restrict__ sum_out, int64_t rows, int cols,
+                       float eps, int ns, int slot_bytes) {
+  using namespace sm100;
+  constexpr int E = Vec<TI>::N;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(ns) * slot_bytes);
+  uint64_t* empty = full + ns;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t nr = max(static_cast<int64_t>(0), min(per, rows - r0));
+  const uint32_t row_bytes = static_cast<uint32_t>(cols) * sizeof(TI);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == STREAM_WARPS) {
+    if (lane == 0) {
+      for (int64_t i = 0; i < nr; ++i) {
+        const int slot = static_cast<int>(i % ns);
+        const uint32_t ph = static_cast<uint32_t>((i / ns) & 1);
+        mbar_wait(&empty[slot], ph ^ 1);
+        uint8_t* dst = smem + static_cast<size_t>(slot) * slot_bytes;
+        mbar_arrive_expect_tx(&full[slot], MODE == 1 && res ? 2 * row_bytes : row_bytes);
+        bulk_load(dst, x + (r0 + i) * cols, row_bytes, &full[slot]);
+        if (MODE == 1 && res) bulk_load(dst + row_bytes, res + (r0 + i) * cols, row_bytes, &full[slot]);
+      }
+    }
+    return;
+  }
+  const int nchunks = cols / E;
+  for (int64_t i = warp; i < nr; i += STREAM_WARPS) {
+    const int slot = static_cast<int>(i % ns);
+    mbar_wait(&full[slot], static_cast<uint32_t>((i / ns) & 1));
+    const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
+    float v[CH][E];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nchunks) {
+        Vec<TI> t;
+        t.u = ld_shared_v4(sx + c * 16);
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[k][e] = OutCvt<TI>::from(t.e[e]);
+        if (MODE == 1 && res) {
+          Vec<TI> r;
+          r.u = ld_shared_v4(sx + row_bytes + c * 16);
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[k][e] += OutCvt<TI>::from(r.e[e]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);  // row consumed: the slot can be refilled
+    const int64_t row = r0 + i;
+    TO* yr = y + row * cols;
+    if constexpr (MODE == 0) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (lane + 32 * k < nchunks)
+#pragma unroll
+          for (int e = 0; e < E; ++e) mx = fmaxf(mx, v[k][e]);
+      mx = warp_max(mx);
+      float sm = 0.0f;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (lane + 32 * k < nchunks)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            v[k][e] = __expf(v[k][e] - mx);
+            sm += v[k][e];
+          }
+      const float inv = 1.0f / warp_sum(sm);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nchunks) {
+          Vec<TO> o;
+#pragma unroll
+          for (int e = 0; e < E; ++e) o.e[e] = OutCvt<TO>::to(v[k][e] * inv);
+          st_stream(yr + c * E, o.u);
+        }
+      }
+    } else {
+      float s = 0.0f;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (lane + 32 * k < nchunks)
+#pragma unroll
+          for (int e = 0; e < E; ++e) s += v[k][e];
+      const float mean = warp_sum(s) / cols;
+      float q = 0.0f;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (lane + 32 * k < nchunks)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const float d = v[k][e] - mean;
+            q = fmaf(d, d, q);
+          }
+      const float rstd = rsqrtf(warp_sum(q) / cols + eps);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nchunks) {
+          Vec<TO> o, so;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int col = c * E + e;
+            o.e[e] = OutCvt<TO>::to((v[k][e] - mean) * rstd * __ldg(gamma + col) + __ldg(beta + col));
+            so.e[e] = OutCvt<TO>::to(v[k][e]);
+          }
+          st_stream(yr + c * E, o.u);
+          if (sum_out) st_stream(sum_out + row * cols + c * E, so.u);
+        }
+      }
+    }
+  }
+}
+
+// Launches the streamed kernel when the shape allows it (16-bit rows whose
+// chunks fit CH <= 16 per lane); returns cudaErrorNotSupported otherwise.
+template <typename TI, typename TO, int MODE>
+cudaError_t stream_launch(const void* x, const void* r, const float* g, const float* b, void* y,
+                          void* so, int64_t rows, int64_t cols, float eps, cudaStream_t s) {
+  constexpr int E = Vec<TI>::N;
+  if (sizeof(TI) != sizeof(TO) || cols % E != 0) return cudaErrorNotSupported;
+  const uintptr_t addr_or = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) |
+                            reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(so);
+  if (addr_or & 15) return cudaErrorNotSupported;
+  const int64_t nchunks = cols / E;
+  const int slot_bytes = static_cast<int>(((MODE == 1 && r ? 2 : 1) * cols * sizeof(TI) + 127) / 128 * 128);
+  const int ns = static_cast<int>(std::min<int64_t>(64, STREAM_SMEM / slot_bytes));
+  if (ns < 4 || rows < 8ll * num_sms()) return cudaErrorNotSupported;
+  const int smem = ns * slot_bytes + ns * 16 + 128;
+  const TI* xi = reinterpret_cast<const TI*>(x);
+  const TI* ri = reinterpret_cast<const TI*>(r);
+  TO* yo = reinterpret_cast<TO*>(y);
+  TO* soo = reinterpret_cast<TO*>(so);
+  const unsigned grid = static_cast<unsigned>(num_sms());
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, (STREAM_WARPS + 1) * 32, smem, s>>>(xi, ri, g, b, yo, soo, rows, (int)cols, eps, ns,
+                                                     slot_bytes);
+    return cudaGetLastError();
+  };
+  cudaError_t e;
+  if (nchunks <= 32) e = go(stream_rows_kernel<TI, TO, MODE, 1>);
+  else if (nchunks <= 64) e = go(stream_rows_kernel<TI, TO, MODE, 2>);
+  else if (nchunks <= 96) e = go(stream_rows_kernel<TI, TO, MODE, 3>);
+  else if (nchunks <= 128) e = go(stream_rows_kernel<TI, TO, MODE, 4>);
+  else if (nchunks <= 256) e = go(stream_rows_kernel<TI, TO, MODE, 8>);
+  else if (nchunks <= 512) e = go(stream_rows_kernel<TI, TO, MODE, 16>);
+  else return cudaErrorNotSupported;
+  count_launch();
+  return e;
 }
 
 // ------------------------------------------------------------ layernorm --
@@ -307,6 +491,10 @@ template <typename T>
 cudaError_t layernorm_launch(const void* x, const void* r, const float* g, const float* b,
                              void* y, void* so, int64_t rows, int64_t cols, float eps,
                              cudaStream_t s) {
+  if (sizeof(T) == 2) {
+    const cudaError_t e = stream_launch<T, T, 1>(x, r, g, b, y, so, rows, cols, eps, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   constexpr int E = Vec<T>::N;
   const uintptr_t addr_or = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) |
                             reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(so);
@@ -333,6 +521,16 @@ cudaError_t layernorm_launch(const void* x, const void* r, const float* g, const
   }
   count_launch();
   return cudaGetLastError();
+}
+
+template <typename TI, typename TO>
+cudaError_t softmax_launch(const void* x, void* y, int64_t rows, int64_t cols, cudaStream_t s) {
+  if (sizeof(TI) == 2 && sizeof(TO) == 2) {
+    const cudaError_t e =
+        stream_launch<TI, TO, 0>(x, nullptr, nullptr, nullptr, y, nullptr, rows, cols, 0.f, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  return softmax_launch_direct<TI, TO>(x, y, rows, cols, s);
 }
 
 // ----------------------------------------------------------- elementwise --

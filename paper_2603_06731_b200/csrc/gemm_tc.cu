@@ -47,6 +47,7 @@ struct GemmTcArgs {
   void* C;
   int num_m_blocks, num_n_blocks;
   int epi;
+  int tma_store;  // 1: stage C through swizzled smem + TMA bulk tensor store
   // implicit-GEMM conv (IM2COL): output pixel m = (n, p, q) over OH x OW,
   // K = KH*KW*C ordered (ky, kx, c) like the OHWI filter.
   int c_blocks, KW, dil_w, dil_h, OH, OW, stride_w, stride_h, lower_w, lower_h;
@@ -57,7 +58,9 @@ struct SmemLayout {
   static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 2;
   static constexpr int B_BYTES = BLOCK_N * BLOCK_K * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;  // 2 x (128 rows x 128 B) C staging
+  static constexpr int EPI_BYTES = 2 * BLOCK_M * 128;
+  static constexpr int BAR_OFFSET = EPI_OFFSET + EPI_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TOTAL = BAR_OFFSET + NUM_BARS * 8 + 16 + 1024;  // +1024 align slack
 };
@@ -132,6 +135,67 @@ __device__ __forceinline__ void store_chunk32(const uint32_t (&acc)[32], const G
   }
 }
 
+// act(acc + bias) (+ residual) for 32 consecutive columns of one row, in fp32.
+template <int EPI, typename OutT>
+__device__ __forceinline__ void epi_values32(const uint32_t (&acc)[32], const GemmTcArgs& a,
+                                             int row, int col0, float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]);
+  if constexpr (EPI != AFG_EPI_NONE) {
+    if (col0 + 32 <= a.N) {
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias + col0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b = __ldg(b4 + j);
+        v[4 * j + 0] += b.x;
+        v[4 * j + 1] += b.y;
+        v[4 * j + 2] += b.z;
+        v[4 * j + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < a.N) v[j] += __ldg(a.bias + col0 + j);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = apply_act<EPI>(v[j]);
+  }
+  if (a.residual != nullptr && row < a.M) {
+    const OutT* rrow = reinterpret_cast<const OutT*>(a.residual) + static_cast<int64_t>(row) * a.ldc + col0;
+    if (col0 + 32 <= a.N && (a.ldc & 7) == 0) {
+      constexpr int PER16 = 16 / sizeof(OutT);
+#pragma unroll
+      for (int j = 0; j < 32 / PER16; ++j) {
+        OutT tmp[PER16];
+        *reinterpret_cast<uint4*>(tmp) = *reinterpret_cast<const uint4*>(rrow + j * PER16);
+#pragma unroll
+        for (int e = 0; e < PER16; ++e) v[j * PER16 + e] += OutCvt<OutT>::from(tmp[e]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < a.N) v[j] += OutCvt<OutT>::from(rrow[j]);
+    }
+  }
+}
+
+template <typename OutT>
+__device__ __forceinline__ void epi_values32_rt(const uint32_t (&acc)[32], const GemmTcArgs& a,
+                                                int row, int col0, float (&v)[32]) {
+  switch (a.epi) {
+    case AFG_EPI_BIAS: epi_values32<AFG_EPI_BIAS, OutT>(acc, a, row, col0, v); break;
+    case AFG_EPI_BIAS_RELU: epi_values32<AFG_EPI_BIAS_RELU, OutT>(acc, a, row, col0, v); break;
+    case AFG_EPI_BIAS_GELU_TANH: epi_values32<AFG_EPI_BIAS_GELU_TANH, OutT>(acc, a, row, col0, v); break;
+    case AFG_EPI_BIAS_GELU_ERF: epi_values32<AFG_EPI_BIAS_GELU_ERF, OutT>(acc, a, row, col0, v); break;
+    default: epi_values32<AFG_EPI_NONE, OutT>(acc, a, row, col0, v); break;
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_out(float a, float b, __nv_bfloat16*) { return pack_bf16(a, b); }
+__device__ __forceinline__ uint32_t pack_out(float a, float b, __half*) { return pack_f16(a, b); }
+
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 template <typename OutT>
 __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], const GemmTcArgs& a,
                                                  int row, int col0) {
@@ -149,7 +213,8 @@ __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], cons
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT, bool IM2COL>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB, const GemmTcArgs args) {
+                   const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, const GemmTcArgs args) {
   using L = SmemLayout<BLOCK_N, STAGES>;
   static_assert(BLOCK_N % 64 == 0 && BLOCK_N <= 256, "BLOCK_N");
   constexpr uint32_t TMEM_COLS = 2 * BLOCK_N <= 32    ? 32
@@ -174,6 +239,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (args.tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -276,27 +342,92 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue --
     const int ew = warp - 4;  // == warp % 4: TMEM lanes [32 ew, 32 ew + 32)
+    const int rloc = ew * 32 + lane;
     int iter = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
-      int mb, nb;
-      tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
-      const int acc = iter & 1;
-      const uint32_t acc_par = (iter >> 1) & 1;
-      mbar_wait(&tfull_bar[acc], acc_par);
-      tc_fence_after();
-      const int row = mb * BLOCK_M + ew * 32 + lane;
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
+    if (args.tma_store) {
+      // C chunk of 128 rows x 128 B staged in 128B-swizzled smem, then one TMA
+      // bulk tensor store; two staging buffers so the store of chunk i
+      // overlaps the TMEM drain of chunk i+1.
+      constexpr int CW = 128 / static_cast<int>(sizeof(OutT));  // columns per chunk
+      uint8_t* stage0 = smem + L::EPI_OFFSET;
+      const bool leader = threadIdx.x == 128;
+      int sb = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+        int mb, nb;
+        tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        const int acc = iter & 1;
+        mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
+        tc_fence_after();
+        const int m0 = mb * BLOCK_M;
+        const int row = m0 + rloc;
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
 #pragma unroll 1
-      for (int c = 0; c < BLOCK_N / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(t_row + c * 32, r);
-        tmem_wait_ld();
-        if (c == BLOCK_N / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&tempty_bar[acc]);
+        for (int cc = 0; cc < BLOCK_N / CW; ++cc) {
+          const int n0 = nb * BLOCK_N + cc * CW;
+          float v[CW];
+#pragma unroll
+          for (int h = 0; h < CW / 32; ++h) {
+            uint32_t r[32];
+            tmem_ld32(t_row + cc * CW + h * 32, r);
+            tmem_wait_ld();
+            float vv[32];
+            epi_values32_rt<OutT>(r, args, row, n0 + h * 32, vv);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[h * 32 + j] = vv[j];
+          }
+          if (cc == BLOCK_N / CW - 1) {
+            tc_fence_before();
+            mbar_arrive(&tempty_bar[acc]);
+          }
+          if (n0 >= args.N) continue;  // uniform across the epilogue warps
+          if (leader) tma_store_wait_read<1>();
+          epi_bar_sync();
+          const uint32_t srow = smem_u32(stage0 + sb * (BLOCK_M * 128) + rloc * 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint32_t w[4];
+            if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                w[k] = pack_out(v[q * 8 + 2 * k], v[q * 8 + 2 * k + 1], static_cast<OutT*>(nullptr));
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(v[q * 4 + k]);
+            }
+            st_shared_v4(srow + ((q ^ (rloc & 7)) * 16), w[0], w[1], w[2], w[3]);
+          }
+          fence_proxy_async_smem();
+          epi_bar_sync();
+          if (leader) {
+            tma_store_2d(&tmC, stage0 + sb * (BLOCK_M * 128), n0, m0);
+            tma_store_commit();
+          }
+          sb ^= 1;
         }
-        const int col0 = nb * BLOCK_N + c * 32;
-        if (col0 < args.N) store_chunk32_rt<OutT>(r, args, row, col0);
+      }
+      if (leader) tma_store_wait<0>();
+    } else {
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+        int mb, nb;
+        tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        const int acc = iter & 1;
+        const uint32_t acc_par = (iter >> 1) & 1;
+        mbar_wait(&tfull_bar[acc], acc_par);
+        tc_fence_after();
+        const int row = mb * BLOCK_M + rloc;
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
+#pragma unroll 1
+        for (int c = 0; c < BLOCK_N / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c * 32, r);
+          tmem_wait_ld();
+          if (c == BLOCK_N / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(&tempty_bar[acc]);
+          }
+          const int col0 = nb * BLOCK_N + c * 32;
+          if (col0 < args.N) store_chunk32_rt<OutT>(r, args, row, col0);
+        }
       }
     }
   }
@@ -314,7 +445,7 @@ __global__ void __launch_bounds__(256, 1)
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT,
           bool IM2COL = false>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const GemmTcArgs& args, cudaStream_t stream) {
+                           const CUtensorMap& tmC, const GemmTcArgs& args, cudaStream_t stream) {
   auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL>;
   constexpr int smem = SmemLayout<BLOCK_N, STAGES>::TOTAL;
   static bool configured = false;  // per-instantiation, per-process
@@ -325,15 +456,16 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
   }
   const int tiles = args.num_m_blocks * args.num_n_blocks;
   const int grid = std::min(tiles, num_sms());
-  kern<<<grid, 256, smem, stream>>>(tmA, tmB, args);
+  kern<<<grid, 256, smem, stream>>>(tmA, tmB, tmC, args);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int BLOCK_N, int STAGES>
 cudaError_t dispatch_types(afg_dtype ab, afg_dtype c, bool b_mn_major, const CUtensorMap& tmA,
-                           const CUtensorMap& tmB, const GemmTcArgs& args, cudaStream_t s) {
-#define AFG_GEMM_V(MN, BF, OT) launch_variant<BLOCK_N, STAGES, MN, BF, OT>(tmA, tmB, args, s)
+                           const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmTcArgs& args,
+                           cudaStream_t s) {
+#define AFG_GEMM_V(MN, BF, OT) launch_variant<BLOCK_N, STAGES, MN, BF, OT>(tmA, tmB, tmC, args, s)
   if (ab == AFG_BF16) {
     if (c == AFG_BF16) return b_mn_major ? AFG_GEMM_V(true, true, __nv_bfloat16)
                                          : AFG_GEMM_V(false, true, __nv_bfloat16);
@@ -347,6 +479,19 @@ cudaError_t dispatch_types(afg_dtype ab, afg_dtype c, bool b_mn_major, const CUt
   }
 #undef AFG_GEMM_V
   return cudaErrorNotSupported;
+}
+
+// TMA store descriptor for C [M, N] (row pitch ldc): boxes of 128 rows x 128 B
+// (64 16-bit or 32 fp32 columns), 128-byte swizzle. 0 if C is not TMA-
+// addressable (then the epilogue stores straight from registers).
+int make_store_map(CUtensorMap* map, void* C, afg_dtype c, int64_t M, int64_t N, int64_t ldc) {
+  const int es = dtype_bytes(c);
+  if ((reinterpret_cast<uintptr_t>(C) & 15) || (ldc * es) % 16 != 0) return 0;
+  const CUtensorMapDataType dt = c == AFG_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : c == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  if (make_tmap_2d(map, C, dt, es, N, M, ldc, 128 / es, BLOCK_M) != AFG_OK) return 0;
+  return 1;
 }
 
 }  // namespace
@@ -381,13 +526,15 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   args.num_m_blocks = static_cast<int>((M + BLOCK_M - 1) / BLOCK_M);
   args.num_n_blocks = static_cast<int>((N + block_n - 1) / block_n);
   args.epi = static_cast<int>(epi);
+  CUtensorMap tmC;
+  args.tma_store = make_store_map(&tmC, C, c, M, N, ldc);
   cudaError_t e;
   if (block_n == 256)
-    e = dispatch_types<256, 4>(ab, c, b_mn_major, tmA, tmB, args, stream);
+    e = dispatch_types<256, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 128)
-    e = dispatch_types<128, 6>(ab, c, b_mn_major, tmA, tmB, args, stream);
+    e = dispatch_types<128, 6>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else
-    e = dispatch_types<64, 8>(ab, c, b_mn_major, tmA, tmB, args, stream);
+    e = dispatch_types<64, 8>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   if (e == cudaErrorNotSupported)
     return set_error(AFG_ERR_UNSUPPORTED, "gemm_tc: unsupported (ab, c) dtype pair");
   return cuda_status(e, "gemm_tc launch");
@@ -445,10 +592,12 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   args.lower_w = lower[0];
   args.lower_h = lower[1];
   cudaError_t e;
-#define AFG_CONV_V(BN, ST)                                                                  \
-  (dt == AFG_BF16 ? launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, args, \
-                                                                            stream)         \
-                  : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, args, stream))
+  CUtensorMap tmC;
+  args.tma_store = make_store_map(&tmC, y, dt, M, OC, OC);
+#define AFG_CONV_V(BN, ST)                                                                    \
+  (dt == AFG_BF16                                                                             \
+       ? launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, tmC, args, stream) \
+       : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, tmC, args, stream))
   if (block_n == 256)
     e = AFG_CONV_V(256, 4);
   else if (block_n == 128)
