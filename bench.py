@@ -128,17 +128,7 @@ def dist_env():
     return rank, world, local
 
 
-def shard_rows(total, rank, world):
-    """Contiguous row shard [begin, end) of `total` rows for `rank`."""
-    base, rem = divmod(total, world)
-    begin = rank * base + min(rank, rem)
-    return begin, begin + base + (1 if rank < rem else 0)
-
-
-def shard_seed(s0, first_element):
-    """Stream state whose draw i equals draw first_element + i of stream s0
-    (splitmix64 advances its state by the golden constant per draw)."""
-    return (s0 + first_element * 0x9E3779B97F4A7C15) & (2**64 - 1)
+from paper_2603_06731_b200.shard import shard_rows, shard_seed  # noqa: E402
 
 
 # ============================================================ workloads ===

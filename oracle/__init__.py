@@ -72,6 +72,7 @@ def lib():
         L.orc_stream_seed.argtypes = [ctypes.c_char_p, ctypes.c_uint64]
         L.orc_random_tensor.argtypes = [_D, _I64, ctypes.c_char_p, ctypes.c_uint64,
                                         ctypes.c_double, ctypes.c_double, _i]
+        L.orc_random_stream.argtypes = [_D, _I64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double]
         L.orc_matmul.argtypes = [_D, _D, _D, _D, _I64, _I64, _I64, _i, _i, _i, _i, _i, _L, _I64, _i]
         L.orc_batch_matmul.argtypes = [_D, _D, _D, _I64, _I64, _I64, _I64]
         L.orc_conv_geometry.argtypes = [_I64] * 8 + [_i, _i, _L]
@@ -126,6 +127,15 @@ def random_tensor(shape, buffer_id: str, seed: int, lo=0.0, hi=1.0, is_int=False
     out = np.empty(n, dtype=np.float64)
     lib().orc_random_tensor(_dp(out), n, buffer_id.encode(), seed & (2**64 - 1), lo, hi,
                             int(is_int))
+    return out.reshape(shape)
+
+
+def random_stream(shape, s0: int, lo=0.0, hi=1.0):
+    """Draws of the splitmix64 stream with state s0 (what afg_fill_uniform
+    generates on the device for seed s0)."""
+    n = int(np.prod(shape)) if len(shape) else 1
+    out = np.empty(n, dtype=np.float64)
+    lib().orc_random_stream(_dp(out), n, s0 & (2**64 - 1), lo, hi)
     return out.reshape(shape)
 
 

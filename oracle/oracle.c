@@ -176,6 +176,16 @@ void orc_random_tensor(double* out, int64_t n, const char* buffer_id, uint64_t s
   }
 }
 
+/* The raw stream from state s0 (s0 = seed ^ hash(id)), for sharded checks. */
+void orc_random_stream(double* out, int64_t n, uint64_t s0, double lo, double hi) {
+  uint64_t state = s0;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t bits = splitmix64(&state);
+    double u = (double)(bits >> 11) * (1.0 / 9007199254740992.0);
+    out[i] = lo + u * (hi - lo);
+  }
+}
+
 /* ------------------------------------------------------- parallel for --- */
 
 typedef void (*range_fn)(void* ctx, int64_t begin, int64_t end);
