@@ -220,6 +220,15 @@ AFG_API afg_status afg_broadcast_in_dim(const void* x, void* y, int in_rank, con
 AFG_API afg_status afg_quantize(const void* x, void* y, int64_t n, float scale, int mode,
                         afg_dtype x_dtype, afg_dtype y_dtype, void* stream);
 
+/* The GEMM epilogue as a standalone pass over an accumulator tile:
+ * out[r, c] = act(acc[r, c] + bias[c]) (+ residual[r, c]), rows x cols,
+ * row pitch ld for acc / residual / out. Used after a split-K reduction
+ * (the fp32 partial sums are reduced across GPUs, then finished here). */
+AFG_API afg_status afg_epilogue_apply(const void* acc, const float* bias, const void* residual,
+                              void* out, int64_t rows, int64_t cols, int64_t ld,
+                              afg_epilogue epi, afg_dtype acc_dtype, afg_dtype out_dtype,
+                              void* stream);
+
 /* Dtype conversion (RNE), used by the graph executor's host staging. */
 AFG_API afg_status afg_convert(const void* x, void* y, int64_t n, afg_dtype x_dtype,
                        afg_dtype y_dtype, void* stream);

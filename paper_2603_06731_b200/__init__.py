@@ -95,6 +95,7 @@ _SIGS = {
     "afg_layernorm_residual": (_i, [_P, _P, _P, _P, _P, _P, _I, _I, _f, _i, _P]),
     "afg_elementwise": (_i, [_P, _P, _P, _I, _I, _i, _i, _i, _i, _P]),
     "afg_reduce_lastdim": (_i, [_P, _P, _I, _I, _i, _i, _i, _P]),
+    "afg_epilogue_apply": (_i, [_P, _P, _P, _P, _I, _I, _I, _i, _i, _i, _P]),
     "afg_convert": (_i, [_P, _P, _I, _i, _i, _P]),
     "afg_transpose": (_i, [_P, _P, _i, _P, _P, _i, _P]),
     "afg_fill_uniform": (_i, [_P, _I, ctypes.c_uint64, _f, _f, _i, _P]),

@@ -624,6 +624,22 @@ __global__ void quantize_kernel(const void* __restrict__ x, void* __restrict__ y
   }
 }
 
+__global__ void epilogue_apply_kernel(const void* __restrict__ acc, const float* __restrict__ bias,
+                                      const void* __restrict__ res, void* __restrict__ out,
+                                      int64_t rows, int64_t cols, int64_t ld, int epi, int adt,
+                                      int odt) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const int64_t idx = r * ld + c;
+    float v = ld_any(acc, idx, adt);
+    if (epi != AFG_EPI_NONE) v = apply_act_rt(epi, v + bias[c]);
+    if (res) v += ld_any(res, idx, odt);
+    st_any(out, idx, odt, v);
+  }
+}
+
 struct TransposeArgs {
   int rank;
   int64_t out_shape[6];
@@ -780,6 +796,19 @@ afg_status afg_broadcast_in_dim(const void* x, void* y, int in_rank, const int64
   broadcast_kernel<<<grid_for(n), 256, 0, s>>>(x, y, n, b, xd, yd);
   count_launch();
   return cuda_status(cudaGetLastError(), "broadcast launch");
+}
+
+afg_status afg_epilogue_apply(const void* acc, const float* bias, const void* residual, void* out,
+                              int64_t rows, int64_t cols, int64_t ld, afg_epilogue epi,
+                              afg_dtype ad, afg_dtype od, void* stream) {
+  if (!acc || !out || rows <= 0 || cols <= 0 || ld < cols || !valid_dt(ad) || !valid_dt(od) ||
+      epi < AFG_EPI_NONE || epi > AFG_EPI_BIAS_GELU_ERF || (epi != AFG_EPI_NONE && !bias))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_epilogue_apply: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  epilogue_apply_kernel<<<grid_for(rows * cols), 256, 0, s>>>(acc, bias, residual, out, rows, cols,
+                                                             ld, epi, ad, od);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "epilogue_apply launch");
 }
 
 afg_status afg_quantize(const void* x, void* y, int64_t n, float scale, int mode, afg_dtype xd,

@@ -91,3 +91,41 @@ def test_gloo_world2_row_sharded_gemm_and_timing():
     assert np.array_equal(C, want)
     assert t == 2.0  # max over ranks
     assert heads == list(range(128))
+
+
+def _splitk_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_06731_b200.tp import gemm_splitk
+        M, K, N = 36, 64, 20
+        A = O.random_tensor((M, K), "%a", 7, -1, 1)
+        B = O.random_tensor((K, N), "%b", 7, -1, 1)
+        k0, k1 = shard_rows(K, rank, world)
+        fn = lambda a, b: torch.from_numpy(O.matmul(a.numpy(), b.numpy()))  # noqa: E731
+        shard = gemm_splitk(torch.from_numpy(A[:, k0:k1].copy()),
+                            torch.from_numpy(B[k0:k1].copy()), partial_fn=fn)
+        out = [None] * world
+        dist.all_gather_object(out, shard.numpy())
+        if rank == 0:
+            q.put(np.concatenate(out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_splitk_reduce_scatter():
+    world, port = 2, free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_splitk_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    C = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = O.random_tensor((36, 64), "%a", 7, -1, 1)
+    B = O.random_tensor((64, 20), "%b", 7, -1, 1)
+    # sum of two f32-rounded half-K partials vs the full product
+    ok, ma, mr, _ = O.compare(C, O.matmul(A, B), 1e-6)
+    assert ok, mr
