@@ -194,7 +194,9 @@ __device__ __forceinline__ void epi_values32_rt(const uint32_t (&acc)[32], const
 __device__ __forceinline__ uint32_t pack_out(float a, float b, __nv_bfloat16*) { return pack_bf16(a, b); }
 __device__ __forceinline__ uint32_t pack_out(float a, float b, __half*) { return pack_f16(a, b); }
 
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar_sync(int g) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+}
 
 template <typename OutT>
 __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], const GemmTcArgs& a,
@@ -211,7 +213,7 @@ __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], cons
 }
 
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT, bool IM2COL>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const GemmTcArgs args) {
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], 256);
     }
     fence_barrier_init();
   }
@@ -341,17 +343,18 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue --
-    const int ew = warp - 4;  // == warp % 4: TMEM lanes [32 ew, 32 ew + 32)
+    // Two groups of 4 warps (warps 4-7 and 8-11); both cover TMEM lanes 0-127
+    // (warp % 4 selects the 32-lane slice) and take alternate column chunks.
+    const int eg = (warp - 4) / 4;
+    const int ew = warp % 4;
     const int rloc = ew * 32 + lane;
     int iter = 0;
     if (args.tma_store) {
-      // C chunk of 128 rows x 128 B staged in 128B-swizzled smem, then one TMA
-      // bulk tensor store; two staging buffers so the store of chunk i
-      // overlaps the TMEM drain of chunk i+1.
+      // C chunk of 128 rows x 128 B staged in 128B-swizzled smem (one buffer
+      // per group), then one TMA bulk tensor store by the group leader.
       constexpr int CW = 128 / static_cast<int>(sizeof(OutT));  // columns per chunk
-      uint8_t* stage0 = smem + L::EPI_OFFSET;
-      const bool leader = threadIdx.x == 128;
-      int sb = 0;
+      uint8_t* stage = smem + L::EPI_OFFSET + eg * (BLOCK_M * 128);
+      const bool leader = ew == 0 && lane == 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
@@ -361,48 +364,56 @@ __global__ void __launch_bounds__(256, 1)
         const int m0 = mb * BLOCK_M;
         const int row = m0 + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
+        const uint32_t srow = smem_u32(stage + rloc * 128);
+        constexpr int NCH = BLOCK_N / CW;
+        if (eg >= NCH) {  // no chunk for this group: still release the accumulator once
+          tc_fence_before();
+          mbar_arrive(&tempty_bar[acc]);
+        }
 #pragma unroll 1
-        for (int cc = 0; cc < BLOCK_N / CW; ++cc) {
+        for (int cc = eg; cc < NCH; cc += 2) {
           const int n0 = nb * BLOCK_N + cc * CW;
-          float v[CW];
+          const bool live = n0 < args.N;  // uniform across the group
+          if (live) {
+            if (leader) tma_store_wait_read<0>();
+            epi_bar_sync(eg);
+          }
 #pragma unroll
           for (int h = 0; h < CW / 32; ++h) {
             uint32_t r[32];
             tmem_ld32(t_row + cc * CW + h * 32, r);
             tmem_wait_ld();
-            float vv[32];
-            epi_values32_rt<OutT>(r, args, row, n0 + h * 32, vv);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[h * 32 + j] = vv[j];
-          }
-          if (cc == BLOCK_N / CW - 1) {
-            tc_fence_before();
-            mbar_arrive(&tempty_bar[acc]);
-          }
-          if (n0 >= args.N) continue;  // uniform across the epilogue warps
-          if (leader) tma_store_wait_read<1>();
-          epi_bar_sync();
-          const uint32_t srow = smem_u32(stage0 + sb * (BLOCK_M * 128) + rloc * 128);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            uint32_t w[4];
-            if constexpr (sizeof(OutT) == 2) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                w[k] = pack_out(v[q * 8 + 2 * k], v[q * 8 + 2 * k + 1], static_cast<OutT*>(nullptr));
-            } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(v[q * 4 + k]);
+            if (h == CW / 32 - 1 && cc + 2 >= NCH) {
+              tc_fence_before();
+              mbar_arrive(&tempty_bar[acc]);  // this thread's last TMEM read of the tile
             }
-            st_shared_v4(srow + ((q ^ (rloc & 7)) * 16), w[0], w[1], w[2], w[3]);
+            if (!live) continue;
+            float v[32];
+            epi_values32_rt<OutT>(r, args, row, n0 + h * 32, v);
+            // 32 values -> 64 B (16-bit) or 128 B (fp32) of the 128 B row
+            constexpr int QPH = 32 * static_cast<int>(sizeof(OutT)) / 16;  // 16 B chunks per half
+#pragma unroll
+            for (int qq = 0; qq < QPH; ++qq) {
+              const int q = h * QPH + qq;
+              uint32_t w[4];
+              if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  w[k] = pack_out(v[qq * 8 + 2 * k], v[qq * 8 + 2 * k + 1], static_cast<OutT*>(nullptr));
+              } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(v[qq * 4 + k]);
+              }
+              st_shared_v4(srow + ((q ^ (rloc & 7)) * 16), w[0], w[1], w[2], w[3]);
+            }
           }
+          if (!live) continue;
           fence_proxy_async_smem();
-          epi_bar_sync();
+          epi_bar_sync(eg);
           if (leader) {
-            tma_store_2d(&tmC, stage0 + sb * (BLOCK_M * 128), n0, m0);
+            tma_store_2d(&tmC, stage, n0, m0);
             tma_store_commit();
           }
-          sb ^= 1;
         }
       }
       if (leader) tma_store_wait<0>();
@@ -417,11 +428,11 @@ __global__ void __launch_bounds__(256, 1)
         const int row = mb * BLOCK_M + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
 #pragma unroll 1
-        for (int c = 0; c < BLOCK_N / 32; ++c) {
+        for (int c = eg; c < BLOCK_N / 32; c += 2) {
           uint32_t r[32];
           tmem_ld32(t_row + c * 32, r);
           tmem_wait_ld();
-          if (c == BLOCK_N / 32 - 1) {
+          if (c + 2 >= BLOCK_N / 32) {
             tc_fence_before();
             mbar_arrive(&tempty_bar[acc]);
           }
@@ -456,7 +467,7 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
   }
   const int tiles = args.num_m_blocks * args.num_n_blocks;
   const int grid = std::min(tiles, num_sms());
-  kern<<<grid, 256, smem, stream>>>(tmA, tmB, tmC, args);
+  kern<<<grid, 384, smem, stream>>>(tmA, tmB, tmC, args);
   count_launch();
   return cudaGetLastError();
 }

@@ -149,3 +149,12 @@ def test_splitk_partials_and_epilogue_apply(cuda):
     c = finish_epilogue(p0 + p1, bias, Epilogue.BIAS_GELU_TANH, torch.bfloat16)
     want = O.round_to(O.matmul(ah, bh, biash, epi=O.EPI_GELU_TANH, out_t=O.F64), O.BF16)
     check(to_host(c), want, 2.0**-7, "split-K + epilogue")
+
+
+@pytest.mark.parametrize("N,out", [(64, torch.bfloat16), (64, torch.float32), (128, torch.bfloat16),
+                                   (256, torch.bfloat16)])
+def test_many_tiles_per_cta(cuda, N, out):
+    """>= 3 tiles per persistent CTA exercises the accumulator double-buffer
+    hand-off (tmem full/empty phases) for every BLOCK_N / staging variant."""
+    M = 148 * 128 * 3 + 77
+    run_case(cuda, M, N, 128, out=out, epi=Epilogue.BIAS_RELU, rows=np.arange(0, M, 997))
