@@ -239,9 +239,11 @@ class GemmFP32:
         self.flops_rank = self.flops_total = 2.0 * n ** 3
         self.alg_bytes_rank = 4.0 * 3 * n * n
 
+    def pre_step(self):
+        self.flush.zero_()  # > L2: evict operands between steps (untimed)
+
     def step(self):
         from paper_2603_06731_b200 import Epilogue
-        self.flush.zero_()  # > L2: evict operands between steps
         self.ops.gemm(self.A, self.B, bias=self.bias, epilogue=Epilogue.BIAS_RELU, out=self.C)
 
     def launches_per_step(self):
@@ -289,6 +291,8 @@ class _Base:
     def e2e_step(self):
         for d, h in self._h:
             d.copy_(h, non_blocking=True)
+        if getattr(self, "pre_step", None):
+            self.pre_step()
         self.step()
         for d, h in self._o:
             h.copy_(d, non_blocking=True)
@@ -334,7 +338,7 @@ class Attention(_Base):
 
     def step(self):
         self.ops.attention(self.q, self.k, self.v, scale=self.D ** -0.5, causal=self.causal,
-                           out_dtype=self.torch.float16)
+                           out=self.o)
 
     def e2e_inputs(self):
         return [self.q, self.k, self.v]
@@ -538,18 +542,15 @@ class MemChain(_Base):
         self.flops_rank = self.alg_bytes_rank
         self.flops_total = self.alg_bytes_rank * rows / n
 
+    def pre_step(self):
+        if self.flush is not None:
+            self.flush.zero_()  # untimed L2 flush (the LN working set fits in L2)
+
     def step(self):
         if self.kind == "softmax":
-            self.ops.softmax(self.x)
+            self.ops.softmax(self.x, out=self.y)
         else:
-            self.flush.zero_()
-            self.ops.layernorm_residual(self.x, self.r, self.g, self.b)
-
-    def kernel_only(self):
-        if self.kind == "softmax":
-            self.ops.softmax(self.x)
-        else:
-            self.ops.layernorm_residual(self.x, self.r, self.g, self.b)
+            self.ops.layernorm_residual(self.x, self.r, self.g, self.b, out=self.y)
 
     def e2e_inputs(self):
         return [self.x] + ([self.r] if self.kind == "layernorm" else [])
@@ -744,40 +745,61 @@ def run_afg(args, wl, rank, world, local):
         return float(t.item())
 
     stream = torch.cuda.current_stream()
+    pre = getattr(wl, "pre_step", None)  # untimed per-step prologue (L2 flush)
     for _ in range(max(args.warmup, 3)):
+        if pre:
+            pre()
         wl.step()
+    torch.cuda.synchronize()
+    # The step is captured once into a CUDA graph and replayed: host/ctypes
+    # launch latency then never leaks into the device timing of short steps.
+    launches0 = afg.launch_count()
+    run = wl.step
+    graph = None
+    if not args.no_graph:
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            wl.step()
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        launches0 = afg.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            wl.step()
+        run = graph.replay
+    launches_per_step = afg.launch_count() - launches0 if graph else None
+    for _ in range(2):
+        if pre:
+            pre()
+        run()
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     launches0 = afg.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        wl.step()
-    ev1.record(stream)
+    for i in range(args.steps):
+        if pre:
+            pre()  # enqueued before the start event: the GPU is busy, timing is exact
+        evs[i][0].record(stream)
+        run()
+        evs[i][1].record(stream)
     barrier()
-    launches = afg.launch_count() - launches0
-    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (launches_per_step * args.steps if graph is not None
+                else afg.launch_count() - launches0)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms) / args.steps
     clk = clocks.stop()
     ms_max = max_over_ranks(ms)
     scale = 1e9 if wl.unit == "GB/s" else 1e12
     value = wl.flops_total / (ms_max * 1e-3) / scale
 
-    # kernel-only duration of the dominant launch (same stream, events), for
-    # the roofline: one extra timed pass without anything else in the step
-    per = []
-    for _ in range(min(args.steps, 5)):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        wl.step() if not hasattr(wl, "kernel_only") else wl.kernel_only()
-        b.record(stream)
-        b.synchronize()
-        per.append(a.elapsed_time(b))
-    k_ms = statistics.median(per)
+    # roofline of the step's kernels on this rank (device time of the step;
+    # single-kernel workloads: exactly the dominant kernel's duration)
+    k_ms = statistics.median(step_ms)
     if wl.bound == "hbm":
         achieved = wl.alg_bytes_rank / (k_ms * 1e-3) / 1e9
         peak, unit = peaks["hbm_gbs"], "GB/s"
@@ -848,6 +870,8 @@ def main():
     ap.add_argument("--all", action="store_true", help="run every workload (one line each)")
     ap.add_argument("--size", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying "
+                    "a captured CUDA graph of the step")
     args = ap.parse_args()
     rank, world, local = dist_env()
     names = sorted(WORKLOADS) if args.all else [args.workload]

@@ -68,6 +68,18 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (x <= 0): Cody-Waite split x = j + f, f in [0,1), cubic
+// least-squares fit of 2^f (max rel err 7.7e-5, below the 16-bit rounding of
+// P), exponent added as an integer. Used for a quarter of the probabilities so
+// the MUFU (ex2) pipe and the FMA pipe share the exponentials.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.0f);
+  const float j = floorf(x);
+  const float f = x - j;
+  const float p = fmaf(fmaf(fmaf(0.077907223f, f, 0.226233534f), f, 0.695776742f), f, 0.999927886f);
+  return __int_as_float(__float_as_int(p) + (__float2int_rn(j) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf16) {
   return bf16 ? pack_bf16(a, b) : pack_f16(a, b);
 }
@@ -282,12 +294,17 @@ __global__ void __launch_bounds__(384, 1)
           for (int e = 0; e < 32; ++e) tmax = fmaxf(tmax, score(sr[e], k0 + c * 32 + e));
         }
       }
-      const float m_new = fmaxf(m, tmax);
+      // lazy rescaling: the running max only moves when it grows by more than
+      // 8 (log2 units; P stays <= 2^8, exact in fp16/bf16 range), so the O
+      // correction below is rare after the first tiles.
+      const float m_cand = fmaxf(m, tmax);
+      const bool upd = m == -INFINITY || m_cand > m + 8.0f;
+      const float m_new = upd ? m_cand : m;
       const float base = m_new == -INFINITY ? 0.0f : m_new;
-      const float alpha = ex2(m - base);  // 0 on the first tile
+      const float alpha = upd ? ex2(m - base) : 1.0f;  // 0 on the first tile
       // correction O *= exp(m_old - m_new) once per tile (warp-uniform decision:
       // tcgen05.ld/st are warp-collective; rows whose max did not move use 1)
-      if (j > 0 && __any_sync(0xffffffffu, m_new > m)) {
+      if (j > 0 && __any_sync(0xffffffffu, upd)) {
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           uint32_t o[32];
@@ -311,8 +328,10 @@ __global__ void __launch_bounds__(384, 1)
         if (fast) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float p0 = ex2(fmaf(__uint_as_float(sr[2 * e]), args.scale_log2, nb));
-            const float p1 = ex2(fmaf(__uint_as_float(sr[2 * e + 1]), args.scale_log2, nb));
+            const float x0 = fmaf(__uint_as_float(sr[2 * e]), args.scale_log2, nb);
+            const float x1 = fmaf(__uint_as_float(sr[2 * e + 1]), args.scale_log2, nb);
+            const float p0 = ex2(x0);
+            const float p1 = (e & 1) ? ex2(x1) : ex2_poly(x1);  // 1/4 on the FMA pipe
             tsum += p0 + p1;
             pk[e] = pack2(p0, p1, BF16);
           }

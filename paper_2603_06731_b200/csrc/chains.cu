@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "afg_internal.h"
 #include "epilogue.cuh"
@@ -210,8 +211,30 @@ cudaError_t softmax_launch_direct(const void* x, void* y, int64_t rows, int64_t 
 // each reduce every 8th row out of shared memory and write the result with
 // coalesced 16-byte stores. In-flight bytes live in shared memory (~160 KB
 // per SM), not in registers, so HBM stays saturated.
-constexpr int STREAM_WARPS = 8;
+constexpr int STREAM_WARPS = 15;  // + 1 producer warp = 16 warps: 128 registers per thread
 constexpr int STREAM_SMEM = 160 * 1024;
+
+__device__ __forceinline__ float ex2f_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// max over the 8 16-bit values of a chunk with packed (x2) compares
+template <typename T>
+__device__ __forceinline__ float chunk_max(const Vec<T>& t) {
+  if constexpr (sizeof(T) == 2) {
+    using T2 = typename std::conditional<std::is_same<T, __half>::value, __half2, __nv_bfloat162>::type;
+    const T2* p = reinterpret_cast<const T2*>(&t.u);
+    T2 m = __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3]));
+    return fmaxf(OutCvt<T>::from(m.x), OutCvt<T>::from(m.y));
+  } else {
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < Vec<T>::N; ++e) m = fmaxf(m, OutCvt<T>::from(t.e[e]));
+    return m;
+  }
+}
 
 template <typename TI, typename TO, int MODE, int CH>  // MODE 0 softmax, 1 layernorm
 __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
@@ -226,6 +249,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
                                              ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(ns) * slot_bytes);
   uint64_t* empty = full + ns;
+  float* gb = reinterpret_cast<float*>(empty + ns);  // layernorm: gamma | beta
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * per;
@@ -238,10 +262,23 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     }
     fence_barrier_init();
   }
+  if constexpr (MODE == 1) {
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      gb[c] = gamma[c];
+      gb[cols + c] = beta[c];
+    }
+  }
   __syncthreads();
   if (warp == STREAM_WARPS) {
-    if (lane == 0) {
-      for (int64_t i = 0; i < nr; ++i) {
+    // The lanes issue a batch of up to 32 rows in parallel (the mbarrier /
+    // bulk-copy issue latency of one row does not serialise the ring), batches
+    // in lock-step: with batch <= ring depth, a row's slot was released by the
+    // row one lap earlier, whose own wait completed in an earlier batch, so the
+    // parity of the empty barrier it waits on is never two phases stale.
+    const int batch = ns < 32 ? ns : 32;
+    for (int64_t b0 = 0; b0 < nr; b0 += batch) {
+      const int64_t i = b0 + lane;
+      if (lane < batch && i < nr) {
         const int slot = static_cast<int>(i % ns);
         const uint32_t ph = static_cast<uint32_t>((i / ns) & 1);
         mbar_wait(&empty[slot], ph ^ 1);
@@ -250,50 +287,40 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         bulk_load(dst, x + (r0 + i) * cols, row_bytes, &full[slot]);
         if (MODE == 1 && res) bulk_load(dst + row_bytes, res + (r0 + i) * cols, row_bytes, &full[slot]);
       }
+      __syncwarp();
     }
     return;
   }
   const int nchunks = cols / E;
+  const uint32_t gb_addr = smem_u32(gb);
   for (int64_t i = warp; i < nr; i += STREAM_WARPS) {
     const int slot = static_cast<int>(i % ns);
     mbar_wait(&full[slot], static_cast<uint32_t>((i / ns) & 1));
     const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
-    float v[CH][E];
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      const int c = lane + 32 * k;
-      if (c < nchunks) {
-        Vec<TI> t;
-        t.u = ld_shared_v4(sx + c * 16);
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[k][e] = OutCvt<TI>::from(t.e[e]);
-        if (MODE == 1 && res) {
-          Vec<TI> r;
-          r.u = ld_shared_v4(sx + row_bytes + c * 16);
-#pragma unroll
-          for (int e = 0; e < E; ++e) v[k][e] += OutCvt<TI>::from(r.e[e]);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);  // row consumed: the slot can be refilled
     const int64_t row = r0 + i;
     TO* yr = y + row * cols;
     if constexpr (MODE == 0) {
+      Vec<TI> raw[CH];
       float mx = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < CH; ++k)
-        if (lane + 32 * k < nchunks)
-#pragma unroll
-          for (int e = 0; e < E; ++e) mx = fmaxf(mx, v[k][e]);
-      mx = warp_max(mx);
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nchunks) {
+          raw[k].u = ld_shared_v4(sx + c * 16);
+          mx = fmaxf(mx, chunk_max<TI>(raw[k]));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // row consumed: the slot can be refilled
+      const float nm = -warp_max(mx) * 1.4426950408889634f;
+      float v[CH][E];
       float sm = 0.0f;
 #pragma unroll
       for (int k = 0; k < CH; ++k)
         if (lane + 32 * k < nchunks)
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            v[k][e] = __expf(v[k][e] - mx);
+            v[k][e] = ex2f_approx(fmaf(OutCvt<TI>::from(raw[k].e[e]), 1.4426950408889634f, nm));
             sm += v[k][e];
           }
       const float inv = 1.0f / warp_sum(sm);
@@ -308,6 +335,25 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
     } else {
+      float v[CH][E];
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nchunks) {
+          Vec<TI> t;
+          t.u = ld_shared_v4(sx + c * 16);
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[k][e] = OutCvt<TI>::from(t.e[e]);
+          if (res) {
+            Vec<TI> r;
+            r.u = ld_shared_v4(sx + row_bytes + c * 16);
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[k][e] += OutCvt<TI>::from(r.e[e]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
       float s = 0.0f;
 #pragma unroll
       for (int k = 0; k < CH; ++k)
@@ -331,10 +377,16 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         if (c < nchunks) {
           Vec<TO> o, so;
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int col = c * E + e;
-            o.e[e] = OutCvt<TO>::to((v[k][e] - mean) * rstd * __ldg(gamma + col) + __ldg(beta + col));
-            so.e[e] = OutCvt<TO>::to(v[k][e]);
+          for (int e = 0; e < E; e += 4) {
+            const uint4 g4 = ld_shared_v4(gb_addr + (c * E + e) * 4);
+            const uint4 b4 = ld_shared_v4(gb_addr + (cols + c * E + e) * 4);
+            const float gg[4] = {__uint_as_float(g4.x), __uint_as_float(g4.y), __uint_as_float(g4.z), __uint_as_float(g4.w)};
+            const float bbv[4] = {__uint_as_float(b4.x), __uint_as_float(b4.y), __uint_as_float(b4.z), __uint_as_float(b4.w)};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              o.e[e + u] = OutCvt<TO>::to(fmaf((v[k][e + u] - mean) * rstd, gg[u], bbv[u]));
+              so.e[e + u] = OutCvt<TO>::to(v[k][e + u]);
+            }
           }
           st_stream(yr + c * E, o.u);
           if (sum_out) st_stream(sum_out + row * cols + c * E, so.u);
@@ -356,9 +408,9 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   if (addr_or & 15) return cudaErrorNotSupported;
   const int64_t nchunks = cols / E;
   const int slot_bytes = static_cast<int>(((MODE == 1 && r ? 2 : 1) * cols * sizeof(TI) + 127) / 128 * 128);
-  const int ns = static_cast<int>(std::min<int64_t>(64, STREAM_SMEM / slot_bytes));
+  const int ns = static_cast<int>(std::min<int64_t>(96, STREAM_SMEM / slot_bytes));
   if (ns < 4 || rows < 8ll * num_sms()) return cudaErrorNotSupported;
-  const int smem = ns * slot_bytes + ns * 16 + 128;
+  const int smem = ns * slot_bytes + ns * 16 + 128 + (MODE == 1 ? static_cast<int>(cols) * 8 + 16 : 0);
   const TI* xi = reinterpret_cast<const TI*>(x);
   const TI* ri = reinterpret_cast<const TI*>(r);
   TO* yo = reinterpret_cast<TO*>(y);
@@ -376,8 +428,7 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   else if (nchunks <= 96) e = go(stream_rows_kernel<TI, TO, MODE, 3>);
   else if (nchunks <= 128) e = go(stream_rows_kernel<TI, TO, MODE, 4>);
   else if (nchunks <= 256) e = go(stream_rows_kernel<TI, TO, MODE, 8>);
-  else if (nchunks <= 512) e = go(stream_rows_kernel<TI, TO, MODE, 16>);
-  else return cudaErrorNotSupported;
+  else return cudaErrorNotSupported;  // longer rows: direct kernels
   count_launch();
   return e;
 }

@@ -67,20 +67,20 @@ def gemm_batched(a, b, out_dtype=None):
     return out
 
 
-def softmax(x, out_dtype=None):
+def softmax(x, out_dtype=None, out=None):
     _need_cuda(x)
     x = x.contiguous()
-    od = out_dtype or x.dtype
-    y = torch.empty(x.shape, dtype=od, device=x.device)
+    od = out_dtype or (out.dtype if out is not None else x.dtype)
+    y = out if out is not None else torch.empty(x.shape, dtype=od, device=x.device)
     cols = x.shape[-1]
     check(lib().afg_softmax_lastdim(_ptr(x), _ptr(y), x.numel() // cols, cols, afg_dtype(x.dtype),
                                     afg_dtype(od), _stream()))
     return y
 
 
-def layernorm_residual(x, residual, gamma, beta, eps=1e-12, sum_out=None):
+def layernorm_residual(x, residual, gamma, beta, eps=1e-12, sum_out=None, out=None):
     _need_cuda(x, residual, gamma, beta)
-    y = torch.empty_like(x)
+    y = out if out is not None else torch.empty_like(x)
     cols = x.shape[-1]
     check(lib().afg_layernorm_residual(_ptr(x), _ptr(residual), _ptr(gamma), _ptr(beta), _ptr(y),
                                        _ptr(sum_out), x.numel() // cols, cols, eps,
@@ -179,13 +179,13 @@ def conv_pack_filter(w_oihw):
     return out
 
 
-def attention(q, k, v, bias=None, scale=1.0, causal=False, out_dtype=None):
+def attention(q, k, v, bias=None, scale=1.0, causal=False, out_dtype=None, out=None):
     """o = softmax(scale q k^T + bias [+causal]) v; q,k,v [B,H,N,D]."""
     _need_cuda(q, k, v, bias)
     B, H, Nq, D = q.shape
     Nk = k.shape[2]
-    od = out_dtype or q.dtype
-    o = torch.empty((B, H, Nq, D), dtype=od, device=q.device)
+    od = out_dtype or (out.dtype if out is not None else q.dtype)
+    o = out if out is not None else torch.empty((B, H, Nq, D), dtype=od, device=q.device)
     check(lib().afg_attention_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(bias), _ptr(o), B, H, Nq, Nk, D,
                                   scale, int(causal), afg_dtype(q.dtype), afg_dtype(od), _stream()))
     return o

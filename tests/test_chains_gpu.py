@@ -25,6 +25,8 @@ def test_fill_uniform_bit_exact_vs_reference_generator(cuda):
 
 @pytest.mark.parametrize("rows,cols,dt,od,tol", [
     (1000, 2048, torch.float16, torch.float16, 2.0**-10),
+    (5003, 2048, torch.float16, torch.float16, 2.0**-10),  # TMA-streamed kernel
+    (6000, 512, torch.bfloat16, torch.bfloat16, 2.0**-7),  # TMA-streamed, short rows
     (257, 512, torch.float32, torch.float32, 1e-5),
     (64, 8192, torch.float16, torch.float32, 1e-5),  # > 4096 cols: block kernel
     (5, 100, torch.bfloat16, torch.bfloat16, 2.0**-7),
@@ -48,6 +50,8 @@ def test_softmax_large_magnitudes_finite(cuda):
 
 @pytest.mark.parametrize("rows,cols,dt,tol", [
     (1024, 768, torch.bfloat16, 2.0**-7),
+    (9001, 768, torch.bfloat16, 2.0**-7),  # TMA-streamed kernel (rows >= 8 per SM)
+    (5000, 1024, torch.float16, 2.0**-10),
     (100, 768, torch.float32, 1e-5),
     (33, 1024, torch.float16, 2.0**-10),
     (7, 5000, torch.float32, 1e-5),  # block kernel
