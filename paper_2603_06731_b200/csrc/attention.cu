@@ -80,6 +80,32 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float2int_rn(j) << 23));
 }
 
+// Blackwell packed fp32x2 FMA / ADD and 3-input max: halve the FMA-pipe work
+// of the softmax (the pipe that bounds it; MUFU ex2 has headroom).
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2split(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf16) {
   return bf16 ? pack_bf16(a, b) : pack_f16(a, b);
 }
@@ -274,14 +300,19 @@ __global__ void __launch_bounds__(384, 1)
       const bool fast = brow == nullptr && !need_mask && args.scale_log2 > 0.0f;
       float tmax = -INFINITY;
       if (fast) {
-#pragma unroll 1
+        // TMEM loads double-buffered: chunk c+1 is in flight while c is reduced
+        uint32_t sa[32], sb[32];
+        tmem_ld32(s_base, sa);
+        tmem_wait_ld();
+#pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
-          uint32_t sr[32];
-          tmem_ld32(s_base + c * 32, sr);
-          tmem_wait_ld();
+          uint32_t(&cur)[32] = (c & 1) ? sb : sa;
+          uint32_t(&nxt)[32] = (c & 1) ? sa : sb;
+          if (c + 1 < BN / 32) tmem_ld32(s_base + (c + 1) * 32, nxt);
 #pragma unroll
           for (int e = 0; e < 32; e += 2)
-            tmax = fmaxf(tmax, fmaxf(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])));
+            tmax = fmax3(tmax, __uint_as_float(cur[e]), __uint_as_float(cur[e + 1]));
+          tmem_wait_ld();
         }
         tmax *= args.scale_log2;
       } else {
@@ -319,22 +350,32 @@ __global__ void __launch_bounds__(384, 1)
       // pass 2: P = exp2(s - m) packed to 16 bit, written over S (cols 16c..)
       float tsum = 0.0f;
       const float nb = -base;
-#pragma unroll 1
+      uint32_t sa2[32], sb2[32];
+      tmem_ld32(s_base, sa2);
+      tmem_wait_ld();
+#pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
-        uint32_t sr[32];
-        tmem_ld32(s_base + c * 32, sr);
-        tmem_wait_ld();
+        uint32_t(&sr)[32] = (c & 1) ? sb2 : sa2;
+        uint32_t(&nxt)[32] = (c & 1) ? sa2 : sb2;
+        // the next S chunk (columns 32(c+1)..) is not overwritten by P chunk c
+        // (columns 16c..16c+15), so it can be loaded ahead
+        if (c + 1 < BN / 32) tmem_ld32(s_base + (c + 1) * 32, nxt);
         uint32_t pk[16];
         if (fast) {
+          const uint64_t sc2 = f2(args.scale_log2, args.scale_log2), nb2 = f2(nb, nb);
+          uint64_t acc2 = f2(0.0f, 0.0f);
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float x0 = fmaf(__uint_as_float(sr[2 * e]), args.scale_log2, nb);
-            const float x1 = fmaf(__uint_as_float(sr[2 * e + 1]), args.scale_log2, nb);
-            const float p0 = ex2(x0);
-            const float p1 = (e & 1) ? ex2(x1) : ex2_poly(x1);  // 1/4 on the FMA pipe
-            tsum += p0 + p1;
+            float x0, x1;
+            f2split(ffma2(f2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, nb2),
+                    x0, x1);
+            const float p0 = ex2(x0), p1 = ex2(x1);
+            acc2 = fadd2(acc2, f2(p0, p1));
             pk[e] = pack2(p0, p1, BF16);
           }
+          float a0, a1;
+          f2split(acc2, a0, a1);
+          tsum += a0 + a1;
         } else {
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -345,6 +386,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
         tmem_st16(s_base + c * 16, pk);
+        tmem_wait_ld();
       }
       tmem_wait_st();
       l = l * alpha + tsum;
