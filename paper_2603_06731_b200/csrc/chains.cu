@@ -408,8 +408,14 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   if (addr_or & 15) return cudaErrorNotSupported;
   const int64_t nchunks = cols / E;
   const int slot_bytes = static_cast<int>(((MODE == 1 && r ? 2 : 1) * cols * sizeof(TI) + 127) / 128 * 128);
-  const int ns = static_cast<int>(std::min<int64_t>(96, STREAM_SMEM / slot_bytes));
-  if (ns < 4 || rows < 8ll * num_sms()) return cudaErrorNotSupported;
+  // Ring depth is a multiple of the consumer-warp count: consumer warp w takes
+  // rows w, w+15, ..., so the row one lap before row i (i - ns) is its own and
+  // was already consumed (loaded) when it waits on row i. Otherwise a warp can
+  // poll slot i % ns while row i - ns's bulk copy is still in flight (copies
+  // complete out of order) and the parity wait passes one phase early.
+  const int ns = static_cast<int>(std::min<int64_t>(90, STREAM_SMEM / slot_bytes)) /
+                 STREAM_WARPS * STREAM_WARPS;
+  if (ns < STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;
   const int smem = ns * slot_bytes + ns * 16 + 128 + (MODE == 1 ? static_cast<int>(cols) * 8 + 16 : 0);
   const TI* xi = reinterpret_cast<const TI*>(x);
   const TI* ri = reinterpret_cast<const TI*>(r);

@@ -104,16 +104,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {
-  printf("afg: mbarrier wait timeout: block (%d,%d) thread %d smem+0x%x parity %u\n",
-         blockIdx.x, blockIdx.y, threadIdx.x, smem_u32(bar), parity);
-  __trap();
-}
-
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// try_wait with cluster-scope acquire: pairs with arrivals released at
+// cluster scope by threads of the peer CTA (mbar_arrive_cluster).
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, 1000000;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -121,7 +129,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint64_t t0 = global_ns();
   uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++polls & 255u) == 0 && global_ns() - t0 > 10000000000ull) mbar_timeout(bar, parity);
+    // a wait that never completes (a pipeline bug) traps after 10 s instead of
+    // hanging the GPU. Inline trap, no printf: a call in the kernel would make
+    // ptxas allocate every setmaxnreg region at the smallest register budget.
+    if ((++polls & 255u) == 0 && global_ns() - t0 > 10000000000ull) asm volatile("trap;");
+  }
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait_cluster(bar, parity)) return;
+  const uint64_t t0 = global_ns();
+  uint32_t polls = 0;
+  while (!mbar_try_wait_cluster(bar, parity)) {
+    if ((++polls & 255u) == 0 && global_ns() - t0 > 10000000000ull) asm volatile("trap;");
   }
 }
 
@@ -167,6 +187,27 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* desc, uint64_
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
       "r"(c2), "r"(c3)
       : "memory");
+}
+
+// 2-CTA (cta_group::2) tile load into this CTA's smem whose completion is
+// signalled on `bar_cluster`, a shared::cluster address that may be the peer
+// CTA's barrier (the leader's full barrier of a CTA pair, see mapa_shared).
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* desc,
+                                                 uint32_t bar_cluster, int32_t c0, int32_t c1,
+                                                 int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".cta_group::2 [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+
+// shared::cluster address of `p`'s counterpart (same offset) in CTA `cta`.
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+  return r;
 }
 
 // 1-D bulk copy global -> shared (bytes multiple of 16, 16-byte aligned).
@@ -316,6 +357,64 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       : "memory");
 }
 
+// 2-CTA D[tmem] (+)= A[tmem] * B[smem] (M = 256; leader CTA issues).
+__device__ __forceinline__ void mma_f16_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Warp-uniform issue variants: the whole MMA warp runs the issue loop (so the
+// descriptors stay in uniform registers) and only the lane with `leader` set
+// issues. `leader` comes from elect_one() once per loop. CG = cta_group.
+template <int CG = 1>
+__device__ __forceinline__ void mma_f16_ss_if(bool leader, uint32_t tmem_d, uint64_t adesc,
+                                              uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::%6.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(static_cast<uint32_t>(leader)),
+      "n"(CG)
+      : "memory");
+}
+template <int CG = 1>
+__device__ __forceinline__ void mma_f16_ts_if(bool leader, uint32_t tmem_d, uint32_t tmem_a,
+                                              uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::%6.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(static_cast<uint32_t>(leader)),
+      "n"(CG)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_if(bool leader, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar)), "r"(static_cast<uint32_t>(leader))
+      : "memory");
+}
+// cta_group::2 commit multicast to the barrier at the same offset in the CTAs of `mask`
+__device__ __forceinline__ void mma_commit_pair_if(bool leader, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %2, 0;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "h"(mask), "r"(static_cast<uint32_t>(leader))
+      : "memory");
+}
+
 // Arrive (once) on `bar` when all previously issued tcgen05 ops of this thread
 // have completed. Implies tcgen05.fence::before_thread_sync.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -426,6 +525,16 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, uint32_
          | (ab_bf16 << 7)          // A format
          | (ab_bf16 << 10)         // B format
          | (a_mn_major << 15) | (b_mn_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// Per-warpgroup register budget (all four warps of a warpgroup execute it).
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 
 // ------------------------------------------------------------------ misc ----

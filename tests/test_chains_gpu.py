@@ -40,6 +40,38 @@ def test_softmax(cuda, rows, cols, dt, od, tol):
     check(to_host(y), want, tol, "softmax")
 
 
+def test_softmax_full_size_streamed_repeat(cuda):
+    # BASELINE's softmax workload at full size ([8*16*2048, 2048] fp16, 1772 rows
+    # per SM through the TMA ring), launched repeatedly: an early pass of a
+    # ring-slot wait shows up as corrupted rows or a hang. Checked against a
+    # torch fp32 softmax of the same fp16 values (1 fp16 ulp).
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.rand((262144, 2048), generator=g, device="cuda") * 8 - 4).half()
+    want = torch.softmax(x.float(), dim=-1)
+    for _ in range(4):
+        y = ops.softmax(x)
+        err = ((y.float() - want).abs() / want.abs().clamp_min(1.0)).max().item()
+        assert err <= 2.0**-10, err
+
+
+def test_layernorm_full_size_streamed_repeat(cuda):
+    # BERT's residual + layernorm at full size ([64*512, 768] bf16) repeatedly,
+    # against a torch fp32 restatement of the oracle formula (1 bf16 ulp).
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = (torch.rand((32768, 768), generator=g, device="cuda") * 2 - 1).bfloat16()
+    r = (torch.rand((32768, 768), generator=g, device="cuda") * 2 - 1).bfloat16()
+    gam = torch.rand(768, generator=g, device="cuda") * 0.2 + 0.9
+    bet = torch.rand(768, generator=g, device="cuda") * 0.2 - 0.1
+    s = x.double() + r.double()
+    mu = s.mean(-1, keepdim=True)
+    var = ((s - mu) ** 2).mean(-1, keepdim=True)
+    want = ((s - mu) / torch.sqrt(var + 1e-12) * gam.double() + bet.double())
+    for _ in range(4):
+        y = ops.layernorm_residual(x, r, gam, bet, eps=1e-12)
+        err = ((y.double() - want).abs() / want.abs().clamp_min(1.0)).max().item()
+        assert err <= 2.0**-7, err
+
+
 def test_softmax_large_magnitudes_finite(cuda):
     # rows with entries up to 80 in magnitude stay finite
     x = torch.linspace(-80, 80, 4096, device="cuda").reshape(4, 1024)
