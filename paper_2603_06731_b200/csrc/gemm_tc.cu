@@ -307,39 +307,45 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
-      constexpr uint32_t idesc =
-          idesc_f16(BLOCK_M, BLOCK_N, AB_BF16 ? 1u : 0u, 0u, B_MN_MAJOR ? 1u : 0u);
-      int stage = 0;
-      uint32_t phase = 0;
-      int iter = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
-        const int acc = iter & 1;
-        const uint32_t acc_par = (iter >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_par ^ 1);
+    // The whole warp walks the loop (barrier waits and descriptor arithmetic
+    // stay warp-uniform, in uniform registers); one elected lane issues. The
+    // per-MMA work is a 64-bit immediate add on each descriptor: a
+    // 128 x BLOCK_N x 16 MMA lasts only BLOCK_N / 2 tensor cycles.
+    const bool leader = elect_one();
+    constexpr uint32_t idesc =
+        idesc_f16(BLOCK_M, BLOCK_N, AB_BF16 ? 1u : 0u, 0u, B_MN_MAJOR ? 1u : 0u);
+    const uint64_t a_desc0 = desc_kmajor_sw128(smem_u32(smem));
+    const uint64_t b_desc0 = B_MN_MAJOR ? desc_mnmajor_sw128(smem_u32(smem + L::A_BYTES), 64 * BLOCK_K * 2)
+                                        : desc_kmajor_sw128(smem_u32(smem + L::A_BYTES));
+    constexpr uint64_t STAGE_STEP = L::STAGE_BYTES >> 4;  // descriptor units (16 B)
+    int stage = 0;
+    uint32_t phase = 0;
+    int iter = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      const int acc = iter & 1;
+      const uint32_t acc_par = (iter >> 1) & 1;
+      mbar_wait(&tempty_bar[acc], acc_par ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * L::STAGE_BYTES);
-          const uint32_t b_addr = a_addr + L::A_BYTES;
+        const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
+        const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
 #pragma unroll
-          for (int k = 0; k < BLOCK_K / 16; ++k) {
-            const uint64_t adesc = desc_kmajor_sw128(a_addr + k * 32);
-            const uint64_t bdesc = B_MN_MAJOR
-                                       ? desc_mnmajor_sw128(b_addr + k * 16 * 128, 64 * BLOCK_K * 2)
-                                       : desc_kmajor_sw128(b_addr + k * 32);
-            mma_f16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          mma_commit(&empty_bar[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int k = 0; k < BLOCK_K / 16; ++k) {
+          const uint64_t boff = B_MN_MAJOR ? static_cast<uint64_t>((k * 16 * 128) >> 4)
+                                           : static_cast<uint64_t>((k * 32) >> 4);
+          mma_f16_ss_if(leader, d_tmem, ad + static_cast<uint64_t>((k * 32) >> 4), bd + boff, idesc,
+                        (kb | k) != 0 ? 1u : 0u);
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_if(leader, &empty_bar[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      mma_commit_if(leader, &tfull_bar[acc]);
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue --
