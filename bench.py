@@ -781,6 +781,10 @@ def run_afg(args, wl, rank, world, local):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     barrier()
+    # hold the GPU in a ~2 ms spin before the first step so the host enqueues
+    # every step (graph replays, events) ahead of the device: no host launch
+    # latency can sit between a step's start and end events
+    torch.cuda._sleep(4_000_000)  # cycles (~2 ms at 1.965 GHz)
     for i in range(args.steps):
         if pre:
             pre()  # enqueued before the start event: the GPU is busy, timing is exact

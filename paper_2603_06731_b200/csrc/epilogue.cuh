@@ -19,7 +19,9 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   // x * sigmoid(2u), u = sqrt(2/pi) (x + 0.044715 x^3): the composite the
   // reference graph API expresses with a size-2 softmax.
   const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
-  return x / (1.0f + __expf(-2.0f * u));
+  // fast reciprocal division (2 ulp): exp overflow -> 1 + e = inf -> 0, the
+  // limit of GELU for large negative x
+  return __fdividef(x, 1.0f + __expf(-2.0f * u));
 }
 
 __device__ __forceinline__ float gelu_erf(float x) {

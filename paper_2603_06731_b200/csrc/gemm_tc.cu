@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "afg_internal.h"
 #include "epilogue.cuh"
@@ -53,10 +54,14 @@ struct GemmTcArgs {
   int c_blocks, KW, dil_w, dil_h, OH, OW, stride_w, stride_h, lower_w, lower_h;
 };
 
-template <int BLOCK_N, int STAGES>
+// PAIR: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile with one
+// cta_group::2 MMA per K step; each CTA stages its 128 rows of A and half of
+// the BLOCK_N rows/columns of B (halving per-SM B traffic in smem and L2).
+template <int BLOCK_N, int STAGES, bool PAIR = false>
 struct SmemLayout {
+  static constexpr int B_ROWS = PAIR ? BLOCK_N / 2 : BLOCK_N;  // B rows staged per CTA
   static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 2;
-  static constexpr int B_BYTES = BLOCK_N * BLOCK_K * 2;
+  static constexpr int B_BYTES = B_ROWS * BLOCK_K * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;  // 2 x (128 rows x 128 B) C staging
   static constexpr int EPI_BYTES = 2 * BLOCK_M * 128;
@@ -212,12 +217,14 @@ __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], cons
   }
 }
 
-template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT, bool IM2COL>
+template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT, bool IM2COL,
+          bool PAIR>
 __global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const GemmTcArgs args) {
-  using L = SmemLayout<BLOCK_N, STAGES>;
+  using L = SmemLayout<BLOCK_N, STAGES, PAIR>;
+  constexpr int TILE_M = PAIR ? 2 * BLOCK_M : BLOCK_M;  // rows per (pair) tile
   static_assert(BLOCK_N % 64 == 0 && BLOCK_N <= 256, "BLOCK_N");
   constexpr uint32_t TMEM_COLS = 2 * BLOCK_N <= 32    ? 32
                                  : 2 * BLOCK_N <= 64  ? 64
@@ -237,6 +244,9 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int cid = PAIR ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int ncl = PAIR ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -248,13 +258,18 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 256);
+      // PAIR: one arrival per epilogue warp of both CTAs (on the leader's)
+      mbar_init(&tempty_bar[s], PAIR ? 16 : 256);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    else tmem_alloc<TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -266,16 +281,23 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = cid; t < num_tiles; t += ncl) {
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        const int m0 = mb * TILE_M + static_cast<int>(rank) * BLOCK_M;
+        const int n0 = nb * BLOCK_N + static_cast<int>(rank) * L::B_ROWS;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], L::STAGE_BYTES);
+          // PAIR: both CTAs' bytes complete on the leader's full barrier
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], (PAIR ? 2 : 1) * L::STAGE_BYTES);
+          const uint32_t fb = PAIR ? mapa_shared(&full_bar[stage], 0) : smem_u32(&full_bar[stage]);
+          auto load2d = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
+            if constexpr (PAIR) tma_load_2d_pair(dst, tm, fb, c0, c1);
+            else tma_load_2d(dst, tm, &full_bar[stage], c0, c1);
+          };
           if constexpr (IM2COL) {
-            const int m0 = mb * BLOCK_M;
             const int q = m0 % args.OW;
             const int p = (m0 / args.OW) % args.OH;
             const int n = m0 / (args.OW * args.OH);
@@ -283,20 +305,26 @@ __global__ void __launch_bounds__(384, 1)
             const int cb = kb - tap * args.c_blocks;
             const int ky = tap / args.KW;
             const int kx = tap - ky * args.KW;
-            tma_load_im2col_4d(sa, &tmA, &full_bar[stage], cb * BLOCK_K,
-                               args.lower_w + q * args.stride_w, args.lower_h + p * args.stride_h,
-                               n, static_cast<uint16_t>(kx * args.dil_w),
-                               static_cast<uint16_t>(ky * args.dil_h));
+            if constexpr (PAIR)
+              tma_load_im2col_4d_pair(sa, &tmA, fb, cb * BLOCK_K,
+                                      args.lower_w + q * args.stride_w,
+                                      args.lower_h + p * args.stride_h, n,
+                                      static_cast<uint16_t>(kx * args.dil_w),
+                                      static_cast<uint16_t>(ky * args.dil_h));
+            else
+              tma_load_im2col_4d(sa, &tmA, &full_bar[stage], cb * BLOCK_K,
+                                 args.lower_w + q * args.stride_w, args.lower_h + p * args.stride_h,
+                                 n, static_cast<uint16_t>(kx * args.dil_w),
+                                 static_cast<uint16_t>(ky * args.dil_h));
           } else {
-            tma_load_2d(sa, &tmA, &full_bar[stage], kb * BLOCK_K, mb * BLOCK_M);
+            load2d(sa, &tmA, kb * BLOCK_K, m0);
           }
           if constexpr (B_MN_MAJOR) {
 #pragma unroll
-            for (int j = 0; j < BLOCK_N / 64; ++j)
-              tma_load_2d(sb + j * (64 * BLOCK_K * 2), &tmB, &full_bar[stage],
-                          nb * BLOCK_N + j * 64, kb * BLOCK_K);
+            for (int j = 0; j < L::B_ROWS / 64; ++j)
+              load2d(sb + j * (64 * BLOCK_K * 2), &tmB, n0 + j * 64, kb * BLOCK_K);
           } else {
-            tma_load_2d(sb, &tmB, &full_bar[stage], kb * BLOCK_K, nb * BLOCK_N);
+            load2d(sb, &tmB, kb * BLOCK_K, n0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -311,9 +339,10 @@ __global__ void __launch_bounds__(384, 1)
     // stay warp-uniform, in uniform registers); one elected lane issues. The
     // per-MMA work is a 64-bit immediate add on each descriptor: a
     // 128 x BLOCK_N x 16 MMA lasts only BLOCK_N / 2 tensor cycles.
+    if (rank == 0) {  // PAIR: the leader CTA issues for both
     const bool leader = elect_one();
     constexpr uint32_t idesc =
-        idesc_f16(BLOCK_M, BLOCK_N, AB_BF16 ? 1u : 0u, 0u, B_MN_MAJOR ? 1u : 0u);
+        idesc_f16(TILE_M, BLOCK_N, AB_BF16 ? 1u : 0u, 0u, B_MN_MAJOR ? 1u : 0u);
     const uint64_t a_desc0 = desc_kmajor_sw128(smem_u32(smem));
     const uint64_t b_desc0 = B_MN_MAJOR ? desc_mnmajor_sw128(smem_u32(smem + L::A_BYTES), 64 * BLOCK_K * 2)
                                         : desc_kmajor_sw128(smem_u32(smem + L::A_BYTES));
@@ -321,10 +350,11 @@ __global__ void __launch_bounds__(384, 1)
     int stage = 0;
     uint32_t phase = 0;
     int iter = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+    for (int t = cid; t < num_tiles; t += ncl, ++iter) {
       const int acc = iter & 1;
       const uint32_t acc_par = (iter >> 1) & 1;
-      mbar_wait(&tempty_bar[acc], acc_par ^ 1);
+      if constexpr (PAIR) mbar_wait_cluster(&tempty_bar[acc], acc_par ^ 1);
+      else mbar_wait(&tempty_bar[acc], acc_par ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -336,16 +366,19 @@ __global__ void __launch_bounds__(384, 1)
         for (int k = 0; k < BLOCK_K / 16; ++k) {
           const uint64_t boff = B_MN_MAJOR ? static_cast<uint64_t>((k * 16 * 128) >> 4)
                                            : static_cast<uint64_t>((k * 32) >> 4);
-          mma_f16_ss_if(leader, d_tmem, ad + static_cast<uint64_t>((k * 32) >> 4), bd + boff, idesc,
-                        (kb | k) != 0 ? 1u : 0u);
+          mma_f16_ss_if<PAIR ? 2 : 1>(leader, d_tmem, ad + static_cast<uint64_t>((k * 32) >> 4),
+                                      bd + boff, idesc, (kb | k) != 0 ? 1u : 0u);
         }
-        mma_commit_if(leader, &empty_bar[stage]);
+        if constexpr (PAIR) mma_commit_pair_if(leader, &empty_bar[stage], 3);
+        else mma_commit_if(leader, &empty_bar[stage]);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      mma_commit_if(leader, &tfull_bar[acc]);
+      if constexpr (PAIR) mma_commit_pair_if(leader, &tfull_bar[acc], 3);
+      else mma_commit_if(leader, &tfull_bar[acc]);
+    }
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue --
@@ -355,27 +388,37 @@ __global__ void __launch_bounds__(384, 1)
     const int ew = warp % 4;
     const int rloc = ew * 32 + lane;
     int iter = 0;
+    // this thread's last TMEM read of accumulator `acc` is done
+    auto release_acc = [&](int acc) {
+      tc_fence_before();
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&tempty_bar[acc]);
+          else mbar_arrive_cluster(&tempty_bar[acc], 0);
+        }
+      } else {
+        mbar_arrive(&tempty_bar[acc]);
+      }
+    };
     if (args.tma_store) {
       // C chunk of 128 rows x 128 B staged in 128B-swizzled smem (one buffer
       // per group), then one TMA bulk tensor store by the group leader.
       constexpr int CW = 128 / static_cast<int>(sizeof(OutT));  // columns per chunk
       uint8_t* stage = smem + L::EPI_OFFSET + eg * (BLOCK_M * 128);
       const bool leader = ew == 0 && lane == 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
         const int acc = iter & 1;
         mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
         tc_fence_after();
-        const int m0 = mb * BLOCK_M;
+        const int m0 = mb * TILE_M + static_cast<int>(rank) * BLOCK_M;
         const int row = m0 + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
         const uint32_t srow = smem_u32(stage + rloc * 128);
         constexpr int NCH = BLOCK_N / CW;
-        if (eg >= NCH) {  // no chunk for this group: still release the accumulator once
-          tc_fence_before();
-          mbar_arrive(&tempty_bar[acc]);
-        }
+        if (eg >= NCH) release_acc(acc);  // no chunk for this group: still release once
 #pragma unroll 1
         for (int cc = eg; cc < NCH; cc += 2) {
           const int n0 = nb * BLOCK_N + cc * CW;
@@ -389,10 +432,7 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t r[32];
             tmem_ld32(t_row + cc * CW + h * 32, r);
             tmem_wait_ld();
-            if (h == CW / 32 - 1 && cc + 2 >= NCH) {
-              tc_fence_before();
-              mbar_arrive(&tempty_bar[acc]);  // this thread's last TMEM read of the tile
-            }
+            if (h == CW / 32 - 1 && cc + 2 >= NCH) release_acc(acc);  // last TMEM read of the tile
             if (!live) continue;
             float v[32];
             epi_values32_rt<OutT>(r, args, row, n0 + h * 32, v);
@@ -424,24 +464,21 @@ __global__ void __launch_bounds__(384, 1)
       }
       if (leader) tma_store_wait<0>();
     } else {
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
         const int acc = iter & 1;
         const uint32_t acc_par = (iter >> 1) & 1;
         mbar_wait(&tfull_bar[acc], acc_par);
         tc_fence_after();
-        const int row = mb * BLOCK_M + rloc;
+        const int row = mb * TILE_M + static_cast<int>(rank) * BLOCK_M + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
 #pragma unroll 1
         for (int c = eg; c < BLOCK_N / 32; c += 2) {
           uint32_t r[32];
           tmem_ld32(t_row + c * 32, r);
           tmem_wait_ld();
-          if (c + 2 >= BLOCK_N / 32) {
-            tc_fence_before();
-            mbar_arrive(&tempty_bar[acc]);
-          }
+          if (c + 2 >= BLOCK_N / 32) release_acc(acc);
           const int col0 = nb * BLOCK_N + c * 32;
           if (col0 < args.N) store_chunk32_rt<OutT>(r, args, row, col0);
         }
@@ -450,21 +487,24 @@ __global__ void __launch_bounds__(384, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the leader's MMAs into the peer's TMEM are done
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+    else tmem_dealloc<TMEM_COLS>(tmem_base);
   }
 }
 
 // --------------------------------------------------------------- host side --
 
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT,
-          bool IM2COL = false>
+          bool IM2COL = false, bool PAIR = false>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmC, const GemmTcArgs& args, cudaStream_t stream) {
-  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL>;
-  constexpr int smem = SmemLayout<BLOCK_N, STAGES>::TOTAL;
+  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL, PAIR>;
+  constexpr int smem = SmemLayout<BLOCK_N, STAGES, PAIR>::TOTAL;
+  static_assert(smem <= 232448, "gemm smem over the 227 KB opt-in limit");
   static bool configured = false;  // per-instantiation, per-process
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -472,17 +512,38 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
     configured = true;
   }
   const int tiles = args.num_m_blocks * args.num_n_blocks;
-  const int grid = std::min(tiles, num_sms());
-  kern<<<grid, 384, smem, stream>>>(tmA, tmB, tmC, args);
-  count_launch();
-  return cudaGetLastError();
+  if constexpr (PAIR) {
+    // persistent CTA pairs (clusters of 2 on one TPC), one per 2 SMs
+    const int clusters = std::min(tiles, num_sms() / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, args);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+  } else {
+    const int grid = std::min(tiles, num_sms());
+    kern<<<grid, 384, smem, stream>>>(tmA, tmB, tmC, args);
+    count_launch();
+    return cudaGetLastError();
+  }
 }
 
-template <int BLOCK_N, int STAGES>
+template <int BLOCK_N, int STAGES, bool PAIR = false>
 cudaError_t dispatch_types(afg_dtype ab, afg_dtype c, bool b_mn_major, const CUtensorMap& tmA,
                            const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmTcArgs& args,
                            cudaStream_t s) {
-#define AFG_GEMM_V(MN, BF, OT) launch_variant<BLOCK_N, STAGES, MN, BF, OT>(tmA, tmB, tmC, args, s)
+#define AFG_GEMM_V(MN, BF, OT) \
+  launch_variant<BLOCK_N, STAGES, MN, BF, OT, false, PAIR>(tmA, tmB, tmC, args, s)
   if (ab == AFG_BF16) {
     if (c == AFG_BF16) return b_mn_major ? AFG_GEMM_V(true, true, __nv_bfloat16)
                                          : AFG_GEMM_V(false, true, __nv_bfloat16);
@@ -511,6 +572,18 @@ int make_store_map(CUtensorMap* map, void* C, afg_dtype c, int64_t M, int64_t N,
   return 1;
 }
 
+// CTA-pair tiles (256 x 256) for BLOCK_N = 256 problems with at least one
+// full wave of pair tiles; AFG_GEMM_PAIR=0 disables them (A/B measurements).
+bool use_pair_tiles(int block_n, int64_t M, int64_t N) {
+  static const bool enabled = [] {
+    const char* e = getenv("AFG_GEMM_PAIR");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!enabled || block_n != 256 || M < 256) return false;
+  const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  return pair_tiles >= num_sms() / 2;
+}
+
 }  // namespace
 
 // Entry used by afg_gemm (api.cpp) and the conv / BERT paths.
@@ -521,6 +594,8 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   const bool b_mn_major = b_layout == AFG_B_KN;
   // BLOCK_N: 256 when N is large enough to fill it, else 128 / 64.
   const int block_n = N >= 256 ? 256 : (N > 64 ? 128 : 64);
+  // 256 x 256 tiles on a CTA pair when there are enough of them to fill the GPU
+  const bool pair = use_pair_tiles(block_n, M, N);
   const CUtensorMapDataType tdt =
       ab == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmA, tmB;
@@ -529,7 +604,7 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   if (b_mn_major)
     st = make_tmap_2d(&tmB, B, tdt, 2, N, K, ldb, 64, BLOCK_K);
   else
-    st = make_tmap_2d(&tmB, B, tdt, 2, K, N, ldb, BLOCK_K, block_n);
+    st = make_tmap_2d(&tmB, B, tdt, 2, K, N, ldb, BLOCK_K, pair ? block_n / 2 : block_n);
   if (st != AFG_OK) return st;
 
   GemmTcArgs args;
@@ -540,13 +615,16 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   args.bias = bias;
   args.residual = residual;
   args.C = C;
-  args.num_m_blocks = static_cast<int>((M + BLOCK_M - 1) / BLOCK_M);
+  const int tile_m = pair ? 2 * BLOCK_M : BLOCK_M;
+  args.num_m_blocks = static_cast<int>((M + tile_m - 1) / tile_m);
   args.num_n_blocks = static_cast<int>((N + block_n - 1) / block_n);
   args.epi = static_cast<int>(epi);
   CUtensorMap tmC;
   args.tma_store = make_store_map(&tmC, C, c, M, N, ldc);
   cudaError_t e;
-  if (block_n == 256)
+  if (pair)
+    e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+  else if (block_n == 256)
     e = dispatch_types<256, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 128)
     e = dispatch_types<128, 6>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);

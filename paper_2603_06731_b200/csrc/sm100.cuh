@@ -242,15 +242,27 @@ __device__ __forceinline__ void tma_load_im2col_4d(void* dst, const void* desc, 
       : "memory");
 }
 
-// 2-CTA (cta_group::2) variant: the completion is signalled on the barrier of
-// the leader CTA of the pair (peer bit of the smem address cleared).
+// 2-CTA (cta_group::2) variants: the load lands in this CTA's smem and its
+// completion is signalled on `bar_cluster`, a shared::cluster address that may
+// be the leader CTA's barrier (mapa_shared(bar, 0)).
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* desc,
-                                                 uint64_t* bar, int32_t c0, int32_t c1) {
-  const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+                                                 uint32_t bar_cluster, int32_t c0, int32_t c1) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::"
-      "complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(desc)), "r"(b), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".cta_group::2 [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_im2col_4d_pair(void* dst, const void* desc,
+                                                        uint32_t bar_cluster, int32_t c, int32_t w,
+                                                        int32_t h, int32_t n, uint16_t off_w,
+                                                        uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      ".cta_group::2 [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(off_w), "h"(off_h)
       : "memory");
 }
 

@@ -158,3 +158,26 @@ def test_many_tiles_per_cta(cuda, N, out):
     hand-off (tmem full/empty phases) for every BLOCK_N / staging variant."""
     M = 148 * 128 * 3 + 77
     run_case(cuda, M, N, 128, out=out, epi=Epilogue.BIAS_RELU, rows=np.arange(0, M, 997))
+
+
+# 256 x 256 tiles on a CTA pair (cta_group::2): BLOCK_N = 256 problems with at
+# least a wave of pair tiles. Ragged M / N, both B layouts, every output type,
+# residual, and >= 3 pair tiles per cluster (accumulator hand-off across both
+# CTAs' epilogues).
+PAIR_ROWS = np.array([0, 127, 128, 255, 256, 2047, 3999])
+
+
+@pytest.mark.parametrize("layout", [Layout.B_KN, Layout.B_NK])
+@pytest.mark.parametrize("out", [torch.bfloat16, torch.float32])
+def test_pair_tiles_ragged(cuda, layout, out):
+    run_case(cuda, 4000, 2300, 704, out=out, layout=layout, rows=PAIR_ROWS)
+
+
+def test_pair_tiles_fp16_residual(cuda):
+    run_case(cuda, 4000, 4352, 512, dt=torch.float16, epi=Epilogue.BIAS, residual=True,
+             rows=PAIR_ROWS)
+
+
+def test_pair_tiles_many_per_cluster(cuda):
+    M = 256 * 74 * 3 + 77
+    run_case(cuda, M, 512, 128, epi=Epilogue.BIAS_RELU, rows=np.arange(0, M, 1013))
