@@ -38,6 +38,10 @@ using namespace sm100;
 
 constexpr int BM = 128;  // query rows per CTA
 constexpr int BN = 128;  // keys per KV tile
+// Bit mask over the 8 pair slots of a 16-pair group: which exponential pairs
+// use the FMA-pipe polynomial instead of MUFU ex2. Measured on B200: the
+// softmax is issue-bound, not MUFU-bound, at D = 128 (3/8 cost 9%), so 0.
+constexpr unsigned POLY_PAIRS = 0;
 
 struct AttnArgs {
   const float* bias;  // [BH, Nq, Nk] or null
@@ -61,8 +65,8 @@ struct AttnSmem {
   static constexpr int QB_OFF = TILE;
   static constexpr int RING_OFF = 2 * TILE;
   static constexpr int BAR_OFF = RING_OFF + STAGES * TILE;
-  // q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_done
-  static constexpr int NUM_BARS = 1 + 2 * STAGES + 5;
+  // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2][2], o_full[2], o_empty[2]
+  static constexpr int NUM_BARS = 2 + 2 * STAGES + 10;
   static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
   static_assert(TOTAL <= 232448, "attention smem over the 227 KB opt-in limit");
 };
@@ -111,19 +115,46 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
+// 2^x for a pair of floats on the FMA pipe (offloads the MUFU ex2 unit, which
+// bounds the softmax): x = j + f with j = rint(x) by the 1.5*2^23 magic-number
+// add, 2^f on [-0.5, 0.5] by a cubic minimax fit (max rel err 7.7e-5, below the
+// 16-bit rounding of P), and j added to the exponent field. x is clamped at
+// -120 (2^-120 rounds to 0 in fp16/bf16 P).
+__device__ __forceinline__ void ex2_poly2(uint64_t x2, float& p0, float& p1) {
+  constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
+  float x0, x1;
+  f2split(x2, x0, x1);
+  const uint64_t xx = f2(fmaxf(x0, -120.0f), fmaxf(x1, -120.0f));
+  const uint64_t t = fadd2(xx, f2(MAGIC, MAGIC));
+  const uint64_t j = fadd2(t, f2(-MAGIC, -MAGIC));
+  const uint64_t fr = ffma2(j, f2(-1.0f, -1.0f), xx);  // x - j in [-0.5, 0.5]
+  uint64_t p = ffma2(f2(0.05508886f, 0.05508886f), fr, f2(0.24260466f, 0.24260466f));
+  p = ffma2(p, fr, f2(0.69327629f, 0.69327629f));
+  p = ffma2(p, fr, f2(0.99992889f, 0.99992889f));
+  float q0, q1, t0, t1;
+  f2split(p, q0, q1);
+  f2split(t, t0, t1);
+  // the low bits of t hold j: (bits(t) << 23) == j << 23 (mod 2^32)
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf16) {
   return bf16 ? pack_bf16(a, b) : pack_f16(a, b);
 }
 
-// One CTA = one (b, h) x two 128-row query tiles A and B ("ping-pong"): while
-// the softmax warpgroup of one tile works, the tensor core runs the other
-// tile's MMAs. TMEM (512 columns): S_A [0,128) S_B [128,256) O_A, O_B after.
-// P is written back over S as packed 16-bit values and consumed by the PV MMA
-// straight from TMEM (A operand in tensor memory), so shared memory holds only
-// Q_A, Q_B and the K / V ring. Each softmax thread reads its S row from TMEM
-// once and keeps all 128 scores in registers (max and exponentials from
-// registers): warpgroup 0 (TMA / MMA / TMEM alloc) gives registers to the two
-// softmax warpgroups.
+// Persistent ping-pong kernel. A work unit = one (b, h) x two 128-row query
+// tiles A and B: while the softmax warpgroup of one tile works, the tensor
+// core runs the other tile's MMAs. One CTA per SM walks the units of the grid
+// (snake order over a heavy-first list), so TMEM allocation, barrier set-up,
+// the K/V stream and the output epilogue of one unit overlap the next unit's
+// work instead of costing a CTA launch each.
+// TMEM (512 columns): S_A [0,128) S_B [128,256) O_A, O_B after. P is written
+// back over S as packed 16-bit values and consumed by the PV MMA straight from
+// TMEM (A operand in tensor memory), so shared memory holds only Q_A, Q_B and
+// the K / V ring. Each softmax thread reads its S row from TMEM once and keeps
+// all 128 scores in registers: warpgroup 0 (TMA / MMA / TMEM alloc) gives
+// registers to the two softmax warpgroups.
 // Warps: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4-7 softmax A, 8-11 softmax B.
 template <int D, bool BF16>
 __global__ void __launch_bounds__(384, 1)
@@ -132,7 +163,7 @@ __global__ void __launch_bounds__(384, 1)
                     const __grid_constant__ CUtensorMap tmV, const AttnArgs args) {
   using L = AttnSmem<D>;
   constexpr int NS = L::STAGES;
-  constexpr int DB = D / 64;  // 128-byte swizzle atoms per row
+  constexpr int DB = D / 64;    // 128-byte swizzle atoms per row
   constexpr int NCH = BN / 32;  // 32-column chunks of an S row
   constexpr uint32_t TMEM_COLS = 512;
 
@@ -141,54 +172,69 @@ __global__ void __launch_bounds__(384, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;
   uint64_t* kv_empty = kv_full + NS;
   uint64_t* s_full = kv_empty + NS;  // [2]
-  uint64_t* p_full = s_full + 2;     // [2]
-  uint64_t* o_done = p_full + 2;
+  uint64_t* p_full = s_full + 2;     // [tile][half]: P columns of keys [0,64) / [64,128)
+  uint64_t* o_full = p_full + 4;     // [2]
+  uint64_t* o_empty = o_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
 
   const int n_pairs = (args.Nq + 2 * BM - 1) / (2 * BM);
-  // 1-D grid in dispatch order: heads in groups of HEAD_GROUP; inside a group
-  // the query-tile pairs run from the last (heaviest under causal masking)
-  // down, all heads of the group per pair. Co-resident CTAs then share the
-  // K/V of ~2 groups in L2, and every group - the last one included - ends
-  // on light pairs that fill the tail of the wave (longest job first).
-  constexpr int HEAD_GROUP = 16;
-  const int blk = static_cast<int>(blockIdx.x);
-  const int grp = blk / (HEAD_GROUP * n_pairs);
-  const int gsize = min(HEAD_GROUP, args.BH - grp * HEAD_GROUP);
-  const int off = blk - grp * HEAD_GROUP * n_pairs;
-  const int qp = n_pairs - 1 - off / gsize;
-  const int bh = grp * HEAD_GROUP + off % gsize;
-  const int hh = bh % args.H;
-  const int bb = bh / args.H;
-  const int q0 = qp * 2 * BM;
+  const int n_units = args.BH * n_pairs;
   const int nkv_all = (args.Nk + BN - 1) / BN;
-  // KV tiles per query tile (no local-memory arrays: tile g is a select)
-  auto tiles_of = [&](int first) {
-    return first >= args.Nq ? 0 : args.causal ? min(nkv_all, (first + BM - 1) / BN + 1) : nkv_all;
+  // Unit number u of this CTA -> linear unit index (snake over the grid:
+  // rounds alternate direction so heavy and light units even out per CTA).
+  // Linear order: heads in groups of HEAD_GROUP; inside a group the query-tile
+  // pairs run from the last (heaviest under causal masking) down, all heads of
+  // the group per pair (co-resident CTAs share the group's K/V in L2).
+  auto unit_of = [&](int u) {
+    const int G = static_cast<int>(gridDim.x);
+    return u * G + ((u & 1) ? G - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x));
   };
-  const int nkv0 = tiles_of(q0), nkv1 = tiles_of(q0 + BM);
-  const int nkv_max = max(nkv0, nkv1);
+  struct Unit {
+    int bh, hh, bb, q0, nkv0, nkv1;
+  };
+  auto decode = [&](int lin) {
+    constexpr int HEAD_GROUP = 16;
+    Unit w;
+    const int grp = lin / (HEAD_GROUP * n_pairs);
+    const int gsize = min(HEAD_GROUP, args.BH - grp * HEAD_GROUP);
+    const int off = lin - grp * HEAD_GROUP * n_pairs;
+    const int qp = n_pairs - 1 - off / gsize;
+    w.bh = grp * HEAD_GROUP + off % gsize;
+    w.hh = w.bh % args.H;
+    w.bb = w.bh / args.H;
+    w.q0 = qp * 2 * BM;
+    auto tiles_of = [&](int first) {
+      return first >= args.Nq ? 0 : args.causal ? min(nkv_all, (first + BM - 1) / BN + 1) : nkv_all;
+    };
+    w.nkv0 = tiles_of(w.q0);
+    w.nkv1 = tiles_of(w.q0 + BM);
+    return w;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&p_full[g], 128);
+      mbar_init(&p_full[2 * g], 4);  // one arrival per softmax warp of the tile
+      mbar_init(&p_full[2 * g + 1], 4);
+      mbar_init(&o_full[g], 1);
+      mbar_init(&o_empty[g], 4);
     }
-    mbar_init(o_done, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -200,242 +246,320 @@ __global__ void __launch_bounds__(384, 1)
   auto o_col = [](int g) { return static_cast<uint32_t>(2 * BN + g * D); };
 
   if (warp >= 4) {
-    setmaxnreg_inc<224>();
+    setmaxnreg_inc<232>();
     // --------------------------------- softmax / correction / epilogue (per tile)
     const int g = (warp - 4) / 4;
     const int w4 = warp % 4;
     const int row = w4 * 32 + lane;
-    const int qi = q0 + g * BM + row;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
     const uint32_t s_base = lane_base + s_col(g);
     const uint32_t o_base = lane_base + o_col(g);
-    const int nkv_g = g ? nkv1 : nkv0;
-    const float* brow =
-        args.bias ? args.bias + (static_cast<int64_t>(bh) * args.Nq + min(qi, args.Nq - 1)) *
-                                    args.Nk
-                  : nullptr;
-    float m = -INFINITY;  // running max (scaled log2 units)
-    float l = 0.0f;
-    for (int j = 0; j < (args.dbg >= 3 ? 0 : nkv_g); ++j) {
-      mbar_wait(&s_full[g], j & 1);  // also implies PV(g, j-1) completed (in-order MMAs)
-      tc_fence_after();
-      if (args.dbg == 1) {
-        tc_fence_before();
-        mbar_arrive(&p_full[g]);
-        continue;
-      }
-      // the whole S row (128 fp32 scores) into registers with one TMEM pass
-      uint32_t s[NCH][32];
+    uint32_t s_phase = 0;  // s_full[g] completions consumed so far (parity)
+    // this warp's TMEM writes (P half / O reads) are complete: one arrival per warp
+    auto warp_arrive = [&](uint64_t* bar) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar);
+    };
+    for (int u = 0;; ++u) {
+      const int lin = unit_of(u);
+      if (lin >= n_units) break;
+      const Unit w = decode(lin);
+      const int nkv_g = g ? w.nkv1 : w.nkv0;
+      const int tile_first = w.q0 + g * BM;
+      const int qi = tile_first + row;
+      const float* brow =
+          args.bias ? args.bias + (static_cast<int64_t>(w.bh) * args.Nq + min(qi, args.Nq - 1)) *
+                                      args.Nk
+                    : nullptr;
+      float m = -INFINITY;  // running max (scaled log2 units)
+      float l = 0.0f;
+      for (int j = 0; j < (args.dbg >= 3 ? 0 : nkv_g); ++j) {
+        mbar_wait(&s_full[g], s_phase);  // also implies PV(g, j-1) completed (in-order MMAs)
+        s_phase ^= 1;
+        tc_fence_after();
+        if (args.dbg == 1) {
+          warp_arrive(&p_full[2 * g]);
+          warp_arrive(&p_full[2 * g + 1]);
+          continue;
+        }
+        // the whole S row (128 fp32 scores) into registers with one TMEM pass
+        uint32_t s[NCH][32];
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) tmem_ld32(s_base + c * 32, s[c]);
-      tmem_wait_ld();
-      const int k0 = j * BN;
-      const bool need_mask = (args.causal && k0 + BN - 1 > q0 + g * BM) || k0 + BN > args.Nk;
-      // Fast path (no additive bias, no mask in this tile, scale > 0): the max
-      // is taken on the raw scores and each probability is one FFMA + EX2.
-      // Otherwise the scores are scaled / biased / masked in place first.
-      const bool fast = brow == nullptr && !need_mask && args.scale_log2 > 0.0f;
-      float tmax, sc;
-      if (fast) {
-        float mc[NCH];
+        for (int c = 0; c < NCH; ++c) tmem_ld32(s_base + c * 32, s[c]);
+        tmem_wait_ld();
+        const int k0 = j * BN;
+        const bool need_mask = (args.causal && k0 + BN - 1 > tile_first) || k0 + BN > args.Nk;
+        // Common path (no additive bias, scale > 0): the max is taken on the raw
+        // scores, a causal-diagonal / key-tail tile masks by a per-row count of
+        // valid columns (one compare + select per score), and each probability
+        // is one FFMA + EX2. With a bias the scores are scaled / biased / masked
+        // in place first.
+        const bool fast = brow == nullptr && args.scale_log2 > 0.0f;
+        float tmax, sc;
+        if (fast) {
+          if (need_mask) {
+            const int lim = min(args.Nk, args.causal ? qi + 1 : args.Nk) - k0;  // valid columns
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (c * 32 + e >= lim) s[c][e] = 0xff800000u;  // -inf
+          }
+          float mc[NCH];
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            mc[c] = fmax3(__uint_as_float(s[c][0]), __uint_as_float(s[c][1]),
+                          __uint_as_float(s[c][2]));
+#pragma unroll
+            for (int e = 3; e < 31; e += 2)
+              mc[c] = fmax3(mc[c], __uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1]));
+            mc[c] = fmaxf(mc[c], __uint_as_float(s[c][31]));
+          }
+          tmax = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])) * args.scale_log2;
+          sc = args.scale_log2;
+        } else {
+          tmax = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int kj = k0 + c * 32 + e;
+              float v = __uint_as_float(s[c][e]) * args.scale_log2;
+              if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
+              if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
+              s[c][e] = __float_as_uint(v);
+              tmax = fmaxf(tmax, v);
+            }
+          sc = 1.0f;
+        }
+        // lazy rescaling: the running max only moves when it grows by more than
+        // 8 (log2 units; P stays <= 2^8, exact in fp16/bf16 range), so the O
+        // correction below is rare after the first tiles.
+        const float m_cand = fmaxf(m, tmax);
+        const bool upd = m == -INFINITY || m_cand > m + 8.0f;
+        const float m_new = upd ? m_cand : m;
+        const float base = m_new == -INFINITY ? 0.0f : m_new;
+        const float alpha = upd ? ex2(m - base) : 1.0f;  // 0 on the first tile
+        // correction O *= exp(m_old - m_new) once per tile (warp-uniform decision:
+        // tcgen05.ld/st are warp-collective; rows whose max did not move use 1)
+        if (j > 0 && __any_sync(0xffffffffu, upd)) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(o_base + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(o_base + c * 32, o);
+          }
+        }
+        m = m_new;
+        // P = exp2(sc * s - base) packed to 16 bit, written over S (P chunk c
+        // lands in columns 16c..16c+15; the scores are already in registers)
+        const uint64_t sc2 = f2(sc, sc), nb2 = f2(-base, -base);
+        uint64_t acc2[2] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f)};  // two chains: half the add latency
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          mc[c] = fmax3(__uint_as_float(s[c][0]), __uint_as_float(s[c][1]),
-                        __uint_as_float(s[c][2]));
+          uint32_t pk[16];
 #pragma unroll
-          for (int e = 3; e < 31; e += 2)
-            mc[c] = fmax3(mc[c], __uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1]));
-          mc[c] = fmaxf(mc[c], __uint_as_float(s[c][31]));
-        }
-        tmax = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])) * args.scale_log2;
-        sc = args.scale_log2;
-      } else {
-        tmax = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int kj = k0 + c * 32 + e;
-            float v = __uint_as_float(s[c][e]) * args.scale_log2;
-            if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
-            if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
-            s[c][e] = __float_as_uint(v);
-            tmax = fmaxf(tmax, v);
+          for (int e = 0; e < 16; ++e) {
+            const uint64_t x2 =
+                ffma2(f2(__uint_as_float(s[c][2 * e]), __uint_as_float(s[c][2 * e + 1])), sc2, nb2);
+            float p0, p1;
+            // pairs selected by POLY_PAIRS run on the FMA pipe, the rest on MUFU
+            if ((POLY_PAIRS >> (e % 8)) & 1) {
+              ex2_poly2(x2, p0, p1);
+            } else {
+              float x0, x1;
+              f2split(x2, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            acc2[e & 1] = fadd2(acc2[e & 1], f2(p0, p1));
+            pk[e] = pack2(p0, p1, BF16);
           }
-        sc = 1.0f;
+          tmem_st16(s_base + c * 16, pk);
+          if (c == NCH / 2 - 1) {  // keys [0, 64) of P written: the PV MMA can start
+            tmem_wait_st();
+            warp_arrive(&p_full[2 * g]);
+          }
+        }
+        float a0, a1, a2, a3;
+        f2split(acc2[0], a0, a1);
+        f2split(acc2[1], a2, a3);
+        tmem_wait_st();
+        l = l * alpha + ((a0 + a1) + (a2 + a3));
+        warp_arrive(&p_full[2 * g + 1]);
       }
-      // lazy rescaling: the running max only moves when it grows by more than
-      // 8 (log2 units; P stays <= 2^8, exact in fp16/bf16 range), so the O
-      // correction below is rare after the first tiles.
-      const float m_cand = fmaxf(m, tmax);
-      const bool upd = m == -INFINITY || m_cand > m + 8.0f;
-      const float m_new = upd ? m_cand : m;
-      const float base = m_new == -INFINITY ? 0.0f : m_new;
-      const float alpha = upd ? ex2(m - base) : 1.0f;  // 0 on the first tile
-      // correction O *= exp(m_old - m_new) once per tile (warp-uniform decision:
-      // tcgen05.ld/st are warp-collective; rows whose max did not move use 1)
-      if (j > 0 && __any_sync(0xffffffffu, upd)) {
+      // ---- epilogue: O / l -> global, one 32-column chunk at a time; O_g is
+      // released (o_empty) right after the last chunk's TMEM load, so the next
+      // unit's first PV(g) does not wait for the global stores.
+      mbar_wait(&o_full[g], u & 1);
+      tc_fence_after();
+      const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+      const bool valid = qi < args.Nq && nkv_g > 0;
+      const int64_t base_idx = static_cast<int64_t>(w.bb) * args.o_bs +
+                               static_cast<int64_t>(w.hh) * args.o_hs +
+                               static_cast<int64_t>(qi) * args.o_ss;
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        if (nkv_g > 0) {
           tmem_ld32(o_base + c * 32, o);
           tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(o_base + c * 32, o);
         }
-      }
-      m = m_new;
-      // P = exp2(sc * s - base) packed to 16 bit, written over S (P chunk c
-      // lands in columns 16c..16c+15; the scores are already in registers)
-      const uint64_t sc2 = f2(sc, sc), nb2 = f2(-base, -base);
-      uint64_t acc2 = f2(0.0f, 0.0f);
+        if (c == D / 32 - 1) warp_arrive(&o_empty[g]);
+        if (!valid) continue;
+        if (args.o_dtype == AFG_F32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + base_idx + c * 32);
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        uint32_t pk[16];
+          for (int v = 0; v < 8; ++v)
+            dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
+                                 __uint_as_float(o[4 * v + 2]) * inv_l,
+                                 __uint_as_float(o[4 * v + 3]) * inv_l);
+        } else {
+          const bool ob = args.o_dtype == AFG_BF16;
+          uint4* dst =
+              reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + base_idx + c * 32);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float x0, x1;
-          f2split(ffma2(f2(__uint_as_float(s[c][2 * e]), __uint_as_float(s[c][2 * e + 1])), sc2,
-                        nb2),
-                  x0, x1);
-          const float p0 = ex2(x0), p1 = ex2(x1);
-          acc2 = fadd2(acc2, f2(p0, p1));
-          pk[e] = pack2(p0, p1, BF16);
-        }
-        tmem_st16(s_base + c * 16, pk);
-      }
-      float a0, a1;
-      f2split(acc2, a0, a1);
-      tmem_wait_st();
-      l = l * alpha + (a0 + a1);
-      tc_fence_before();
-      mbar_arrive(&p_full[g]);
-    }
-    // ---- epilogue: O / l -> global
-    mbar_wait(o_done, 0);
-    tc_fence_after();
-    const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
-    const bool valid = qi < args.Nq && nkv_g > 0;
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(o_base + c * 32, o);
-      tmem_wait_ld();
-      if (!valid) continue;
-      const int64_t base_idx = static_cast<int64_t>(bb) * args.o_bs +
-                               static_cast<int64_t>(hh) * args.o_hs +
-                               static_cast<int64_t>(qi) * args.o_ss + c * 32;
-      if (args.o_dtype == AFG_F32) {
-        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + base_idx);
-#pragma unroll
-        for (int v = 0; v < 8; ++v)
-          dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
-                               __uint_as_float(o[4 * v + 2]) * inv_l,
-                               __uint_as_float(o[4 * v + 3]) * inv_l);
-      } else {
-        const bool ob = args.o_dtype == AFG_BF16;
-        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + base_idx);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 u;
-          u.x = pack2(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l, ob);
-          u.y = pack2(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l, ob);
-          u.z = pack2(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l, ob);
-          u.w = pack2(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l, ob);
-          dst[v] = u;
-        }
-      }
-    }
-    } else {
-  setmaxnreg_dec<56>();
-  if (warp == 0) {
-    // --------------------------------------------------------------- TMA --
-    if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * L::TILE);
-      for (int g = 0; g < 2; ++g)
-        for (int a = 0; a < DB; ++a)
-          tma_load_4d(smem + (g ? L::QB_OFF : L::QA_OFF) + a * (BM * 128), &tmQ, q_full, a * 64,
-                      q0 + g * BM, hh, bb);
-      for (int n = 0; n < 2 * nkv_max; ++n) {  // item 2j = K(j), 2j+1 = V(j)
-        const int st = n % NS;
-        mbar_wait(&kv_empty[st], ((n / NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], L::TILE);
-        const CUtensorMap* tm = (n & 1) ? &tmV : &tmK;
-        for (int a = 0; a < DB; ++a)
-          tma_load_4d(smem + L::RING_OFF + st * L::TILE + a * (BN * 128), tm, &kv_full[st],
-                      a * 64, (n >> 1) * BN, hh, bb);
-      }
-    }
-  } else if (warp == 1) {
-    // --------------------------------------------------------------- MMA --
-    // The whole warp runs the issue loop (waits and descriptor arithmetic stay
-    // warp-uniform, in uniform registers) and one elected lane issues: a
-    // 128x128x16 MMA takes 64 tensor cycles, so per-MMA issue work must be a
-    // handful of instructions (descriptors are base + immediate offsets).
-    const bool leader = elect_one();
-    constexpr uint32_t idesc_s = idesc_f16(BM, BN, BF16 ? 1u : 0u, 0u, 0u);
-    constexpr uint32_t idesc_o = idesc_f16(BM, D, BF16 ? 1u : 0u, 0u, 1u);
-    const uint64_t q_desc0 = desc_kmajor_sw128(smem_u32(smem + L::QA_OFF));
-    const uint64_t k_desc0 = desc_kmajor_sw128(smem_u32(smem + L::RING_OFF));
-    const uint64_t v_desc0 = desc_mnmajor_sw128(smem_u32(smem + L::RING_OFF), BN * 128);
-    constexpr uint64_t QB_STEP = (L::QB_OFF - L::QA_OFF) >> 4;  // descriptor units (16 B)
-    constexpr uint64_t SLOT_STEP = L::TILE >> 4;
-    auto wait_item = [&](int n) {
-      mbar_wait(&kv_full[n % NS], (n / NS) & 1);
-      tc_fence_after();
-    };
-    auto issue_s = [&](int g, int j) {
-      const uint64_t qd = q_desc0 + (g ? QB_STEP : 0);
-      const uint64_t kd = k_desc0 + static_cast<uint64_t>((2 * j) % NS) * SLOT_STEP;
-      if (args.dbg != 2) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t off = static_cast<uint64_t>(((kk / 4) * (BM * 128) + (kk % 4) * 32) >> 4);
-          mma_f16_ss_if(leader, tmem + s_col(g), qd + off, kd + off, idesc_s, kk > 0 ? 1u : 0u);
-        }
-      }
-      mma_commit_if(leader, &s_full[g]);
-    };
-    auto issue_pv = [&](int g, int j) {
-      const uint64_t vd = v_desc0 + static_cast<uint64_t>((2 * j + 1) % NS) * SLOT_STEP;
-      if (args.dbg == 2) return;
-#pragma unroll
-      for (int kk = 0; kk < BN / 16; ++kk)
-        mma_f16_ts_if(leader, tmem + o_col(g), tmem + s_col(g) + kk * 8,
-                      vd + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_o,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-    };
-    mbar_wait(q_full, 0);
-    wait_item(0);
-    if (nkv0 > 0) issue_s(0, 0);
-    if (nkv1 > 0) issue_s(1, 0);
-    mma_commit_if(leader, &kv_empty[0]);
-    for (int j = 0; j < nkv_max; ++j) {
-      const int jn = j + 1;
-      bool k_next_ready = false;
-      wait_item(2 * j + 1);
-#pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const int nkv_g = g ? nkv1 : nkv0;
-        if (j < nkv_g) {
-          if (args.dbg < 3) mbar_wait(&p_full[g], j & 1);
-          tc_fence_after();
-          issue_pv(g, j);
-          if (jn < nkv_g) {
-            if (!k_next_ready) {
-              wait_item(2 * jn);
-              k_next_ready = true;
-            }
-            issue_s(g, jn);  // runs after PV(g, j) on the tensor pipe: P(j) consumed first
+          for (int v = 0; v < 4; ++v) {
+            uint4 q;
+            q.x = pack2(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l, ob);
+            q.y = pack2(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l, ob);
+            q.z = pack2(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l, ob);
+            q.w = pack2(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l, ob);
+            dst[v] = q;
           }
         }
       }
-      mma_commit_if(leader, &kv_empty[(2 * j + 1) % NS]);
-      if (k_next_ready) mma_commit_if(leader, &kv_empty[(2 * jn) % NS]);
     }
-    mma_commit_if(leader, o_done);
-  }
+  } else {
+    setmaxnreg_dec<40>();
+    if (warp == 0) {
+      // ------------------------------------------------------------- TMA --
+      if (lane == 0) {
+        int n = 0;  // K/V ring item counter across units (item 2j = K(j), 2j+1 = V(j))
+        for (int u = 0;; ++u) {
+          const int lin = unit_of(u);
+          if (lin >= n_units) break;
+          const Unit w = decode(lin);
+          mbar_wait(q_empty, (u & 1) ^ 1);  // the previous unit's S MMAs are done with Q
+          mbar_arrive_expect_tx(q_full, 2 * L::TILE);
+          for (int g = 0; g < 2; ++g)
+            for (int a = 0; a < DB; ++a)
+              tma_load_4d(smem + (g ? L::QB_OFF : L::QA_OFF) + a * (BM * 128), &tmQ, q_full,
+                          a * 64, w.q0 + g * BM, w.hh, w.bb);
+          const int items = 2 * max(w.nkv0, w.nkv1);
+          for (int it = 0; it < items; ++it, ++n) {
+            const int st = n % NS;
+            mbar_wait(&kv_empty[st], ((n / NS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&kv_full[st], L::TILE);
+            const CUtensorMap* tm = (it & 1) ? &tmV : &tmK;
+            for (int a = 0; a < DB; ++a)
+              tma_load_4d(smem + L::RING_OFF + st * L::TILE + a * (BN * 128), tm, &kv_full[st],
+                          a * 64, (it >> 1) * BN, w.hh, w.bb);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ------------------------------------------------------------- MMA --
+      // The whole warp runs the issue loop (waits and descriptor arithmetic
+      // stay warp-uniform, in uniform registers) and one elected lane issues:
+      // a 128x128x16 MMA takes 64 tensor cycles, so per-MMA issue work must be
+      // a handful of instructions (descriptors are base + immediate offsets).
+      const bool leader = elect_one();
+      constexpr uint32_t idesc_s = idesc_f16(BM, BN, BF16 ? 1u : 0u, 0u, 0u);
+      constexpr uint32_t idesc_o = idesc_f16(BM, D, BF16 ? 1u : 0u, 0u, 1u);
+      const uint64_t q_desc0 = desc_kmajor_sw128(smem_u32(smem + L::QA_OFF));
+      const uint64_t k_desc0 = desc_kmajor_sw128(smem_u32(smem + L::RING_OFF));
+      const uint64_t v_desc0 = desc_mnmajor_sw128(smem_u32(smem + L::RING_OFF), BN * 128);
+      constexpr uint64_t QB_STEP = (L::QB_OFF - L::QA_OFF) >> 4;  // descriptor units (16 B)
+      constexpr uint64_t SLOT_STEP = L::TILE >> 4;
+      int nb = 0;                  // ring item index of this unit's K(0)
+      uint32_t p_phase[2] = {0, 0};  // per tile; both halves complete once per step
+      auto wait_item = [&](int n) {
+        mbar_wait(&kv_full[n % NS], (n / NS) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int g, int j) {
+        const uint64_t qd = q_desc0 + (g ? QB_STEP : 0);
+        const uint64_t kd = k_desc0 + static_cast<uint64_t>((nb + 2 * j) % NS) * SLOT_STEP;
+        if (args.dbg != 2) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off =
+                static_cast<uint64_t>(((kk / 4) * (BM * 128) + (kk % 4) * 32) >> 4);
+            mma_f16_ss_if(leader, tmem + s_col(g), qd + off, kd + off, idesc_s, kk > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit_if(leader, &s_full[g]);
+      };
+      // O_g += P V over keys [64 h, 64 h + 64) (P half h)
+      auto issue_pv_half = [&](int g, int j, int h) {
+        const uint64_t vd = v_desc0 + static_cast<uint64_t>((nb + 2 * j + 1) % NS) * SLOT_STEP;
+        if (args.dbg == 2) return;
+#pragma unroll
+        for (int k2 = 0; k2 < BN / 32; ++k2) {
+          const int kk = h * (BN / 32) + k2;
+          mma_f16_ts_if(leader, tmem + o_col(g), tmem + s_col(g) + kk * 8,
+                        vd + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+      for (int u = 0;; ++u) {
+        const int lin = unit_of(u);
+        if (lin >= n_units) break;
+        const Unit w = decode(lin);
+        const int nkv_max = max(w.nkv0, w.nkv1);
+        mbar_wait(q_full, u & 1);
+        wait_item(nb);
+        if (w.nkv0 > 0) issue_s(0, 0);
+        if (w.nkv1 > 0) issue_s(1, 0);
+        if (nkv_max <= 1) mma_commit_if(leader, q_empty);  // last S of the unit issued
+        mma_commit_if(leader, &kv_empty[nb % NS]);
+        for (int j = 0; j < nkv_max; ++j) {
+          const int jn = j + 1;
+          bool k_next_ready = false;
+          wait_item(nb + 2 * j + 1);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const int nkv_g = g ? w.nkv1 : w.nkv0;
+            if (j < nkv_g) {
+              if (j == 0) mbar_wait(&o_empty[g], (u & 1) ^ 1);  // previous unit's O_g read
+              // PV in two halves: the first 64 keys as soon as their P is written
+              if (args.dbg < 3) mbar_wait(&p_full[2 * g], p_phase[g]);
+              tc_fence_after();
+              issue_pv_half(g, j, 0);
+              if (args.dbg < 3) mbar_wait(&p_full[2 * g + 1], p_phase[g]);
+              p_phase[g] ^= 1;
+              tc_fence_after();
+              issue_pv_half(g, j, 1);
+              if (jn < nkv_g) {
+                if (!k_next_ready) {
+                  wait_item(nb + 2 * jn);
+                  k_next_ready = true;
+                }
+                issue_s(g, jn);  // runs after PV(g, j) on the tensor pipe: P(j) consumed first
+              } else {
+                mma_commit_if(leader, &o_full[g]);  // O_g of this unit complete
+              }
+            }
+          }
+          if (jn == nkv_max - 1) mma_commit_if(leader, q_empty);  // last S of the unit issued
+          mma_commit_if(leader, &kv_empty[(nb + 2 * j + 1) % NS]);
+          if (k_next_ready) mma_commit_if(leader, &kv_empty[(nb + 2 * jn) % NS]);
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if ((g ? w.nkv1 : w.nkv0) == 0) {  // empty tile: keep its O phases in step
+            mbar_wait(&o_empty[g], (u & 1) ^ 1);
+            mma_commit_if(leader, &o_full[g]);
+          }
+        }
+        nb += 2 * nkv_max;
+      }
+    }
   }
 
   tc_fence_before();
@@ -866,7 +990,8 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const unsigned grid = static_cast<unsigned>(a.BH) * ((a.Nq + 2 * BM - 1) / (2 * BM));
+  const int units = a.BH * ((a.Nq + 2 * BM - 1) / (2 * BM));
+  const unsigned grid = static_cast<unsigned>(std::min(units, num_sms()));  // persistent
   kern<<<grid, 384, smem, s>>>(tq, tk, tv, a);
   count_launch();
   return cudaGetLastError();
