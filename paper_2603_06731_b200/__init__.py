@@ -25,7 +25,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libafg.so")
+# AFG_LIB_PATH: load another build of the same library (A/B measurements)
+lib_path = os.environ.get("AFG_LIB_PATH") or os.path.join(_HERE, "libafg.so")
 
 
 class AfgError(RuntimeError):

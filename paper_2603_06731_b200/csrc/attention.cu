@@ -40,8 +40,9 @@ constexpr int BM = 128;  // query rows per CTA
 constexpr int BN = 128;  // keys per KV tile
 // Bit mask over the 8 pair slots of a 16-pair group: which exponential pairs
 // use the FMA-pipe polynomial instead of MUFU ex2. Measured on B200: the
-// softmax is issue-bound, not MUFU-bound, at D = 128 (3/8 cost 9%), so 0.
-constexpr unsigned POLY_PAIRS = 0;
+// MUFU (16 ex2 / clk / SM) and the issue slots balance at 2 pairs in 8
+// (+4% at D = 128); 3/8 and above spill and lose 10%.
+constexpr unsigned POLY_PAIRS = 0x12;
 
 struct AttnArgs {
   const float* bias;  // [BH, Nq, Nk] or null

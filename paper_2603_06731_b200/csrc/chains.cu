@@ -292,103 +292,200 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     return;
   }
   const int nchunks = cols / E;
-  const uint32_t gb_addr = smem_u32(gb);
-  for (int64_t i = warp; i < nr; i += STREAM_WARPS) {
-    const int slot = static_cast<int>(i % ns);
-    mbar_wait(&full[slot], static_cast<uint32_t>((i / ns) & 1));
-    const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
-    const int64_t row = r0 + i;
-    TO* yr = y + row * cols;
-    if constexpr (MODE == 0) {
+  if constexpr (MODE == 0) {
+    for (int64_t i = warp; i < nr; i += STREAM_WARPS) {
+      const int slot = static_cast<int>(i % ns);
+      mbar_wait(&full[slot], static_cast<uint32_t>((i / ns) & 1));
+      const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
+      const int64_t row = r0 + i;
+      TO* yr = y + row * cols;
       Vec<TI> raw[CH];
-      float mx = -INFINITY;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int c = lane + 32 * k;
+          if (c < nchunks) {
+            raw[k].u = ld_shared_v4(sx + c * 16);
+            mx = fmaxf(mx, chunk_max<TI>(raw[k]));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // row consumed: the slot can be refilled
+        const float nm = -warp_max(mx) * 1.4426950408889634f;
+        float v[CH][E];
+        float sm = 0.0f;
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+          if (lane + 32 * k < nchunks)
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              v[k][e] = ex2f_approx(fmaf(OutCvt<TI>::from(raw[k].e[e]), 1.4426950408889634f, nm));
+              sm += v[k][e];
+            }
+        const float inv = 1.0f / warp_sum(sm);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int c = lane + 32 * k;
+          if (c < nchunks) {
+            Vec<TO> o;
+#pragma unroll
+            for (int e = 0; e < E; ++e) o.e[e] = OutCvt<TO>::to(v[k][e] * inv);
+            st_stream(yr + c * E, o.u);
+          }
+        }
+    }
+  } else {
+    // residual + layernorm, two rows per warp at a time (rows i and i + 15 of
+    // this warp's stride): the two rows' reduction chains interleave, which
+    // hides the shuffle / smem latency a single row per warp leaves exposed.
+    // Needs ns >= R * STREAM_WARPS (checked at launch) so the rows sit in
+    // different ring slots.
+    constexpr int R = CH <= 4 ? 2 : 1;  // long rows: one at a time (registers)
+    const uint32_t gb_addr = smem_u32(gb);
+    // a lane always owns the same columns (chunks lane + 32 k): its gamma / beta
+    // live in registers for the whole kernel (rows of <= 768 16-bit columns)
+    constexpr bool GB_REGS = CH <= 3;
+    float greg[GB_REGS ? CH : 1][E], breg[GB_REGS ? CH : 1][E];
+    if constexpr (GB_REGS) {
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int c = lane + 32 * k;
-        if (c < nchunks) {
-          raw[k].u = ld_shared_v4(sx + c * 16);
-          mx = fmaxf(mx, chunk_max<TI>(raw[k]));
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          uint4 g4 = make_uint4(0, 0, 0, 0), b4 = make_uint4(0, 0, 0, 0);
+          if (c < nchunks) {
+            g4 = ld_shared_v4(gb_addr + (c * E + e) * 4);
+            b4 = ld_shared_v4(gb_addr + (cols + c * E + e) * 4);
+          }
+          greg[k][e] = __uint_as_float(g4.x); greg[k][e + 1] = __uint_as_float(g4.y);
+          greg[k][e + 2] = __uint_as_float(g4.z); greg[k][e + 3] = __uint_as_float(g4.w);
+          breg[k][e] = __uint_as_float(b4.x); breg[k][e + 1] = __uint_as_float(b4.y);
+          breg[k][e + 2] = __uint_as_float(b4.z); breg[k][e + 3] = __uint_as_float(b4.w);
+        }
+      }
+    }
+    for (int64_t i0 = warp; i0 < nr; i0 += STREAM_WARPS * R) {
+      float v[R][CH][E];
+      bool have[R];
+      int slot[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t i = i0 + r * STREAM_WARPS;
+        have[r] = i < nr;
+        slot[r] = static_cast<int>(i % ns);
+        if (!have[r]) continue;
+        mbar_wait(&full[slot[r]], static_cast<uint32_t>((i / ns) & 1));
+        const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot[r]) * slot_bytes);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int c = lane + 32 * k;
+          if (c < nchunks) {
+            Vec<TI> t;
+            t.u = ld_shared_v4(sx + c * 16);
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[r][k][e] = OutCvt<TI>::from(t.e[e]);
+            if (res) {
+              Vec<TI> q;
+              q.u = ld_shared_v4(sx + row_bytes + c * 16);
+#pragma unroll
+              for (int e = 0; e < E; ++e) v[r][k][e] += OutCvt<TI>::from(q.e[e]);
+            }
+          }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);  // row consumed: the slot can be refilled
-      const float nm = -warp_max(mx) * 1.4426950408889634f;
-      float v[CH][E];
-      float sm = 0.0f;
+      if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k < CH; ++k)
-        if (lane + 32 * k < nchunks)
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            v[k][e] = ex2f_approx(fmaf(OutCvt<TI>::from(raw[k].e[e]), 1.4426950408889634f, nm));
-            sm += v[k][e];
-          }
-      const float inv = 1.0f / warp_sum(sm);
-#pragma unroll
-      for (int k = 0; k < CH; ++k) {
-        const int c = lane + 32 * k;
-        if (c < nchunks) {
-          Vec<TO> o;
-#pragma unroll
-          for (int e = 0; e < E; ++e) o.e[e] = OutCvt<TO>::to(v[k][e] * inv);
-          st_stream(yr + c * E, o.u);
-        }
+        for (int r = 0; r < R; ++r)
+          if (have[r]) mbar_arrive(&empty[slot[r]]);  // rows consumed: slots refill
       }
-    } else {
-      float v[CH][E];
+      // sums as short trees (one partial per chunk), both rows' shuffles interleaved
+      float s[R], q[R], mean[R], rstd[R];
 #pragma unroll
-      for (int k = 0; k < CH; ++k) {
-        const int c = lane + 32 * k;
-        if (c < nchunks) {
-          Vec<TI> t;
-          t.u = ld_shared_v4(sx + c * 16);
+      for (int r = 0; r < R; ++r) {
+        float part[CH];
 #pragma unroll
-          for (int e = 0; e < E; ++e) v[k][e] = OutCvt<TI>::from(t.e[e]);
-          if (res) {
-            Vec<TI> r;
-            r.u = ld_shared_v4(sx + row_bytes + c * 16);
+        for (int k = 0; k < CH; ++k) {
+          part[k] = 0.0f;
+          if (lane + 32 * k < nchunks) {
+            float a = v[r][k][0] + v[r][k][1], b = v[r][k][2] + v[r][k][3];
 #pragma unroll
-            for (int e = 0; e < E; ++e) v[k][e] += OutCvt<TI>::from(r.e[e]);
+            for (int e = 4; e < E; e += 4) {
+              a += v[r][k][e] + v[r][k][e + 1];
+              b += v[r][k][e + 2] + v[r][k][e + 3];
+            }
+            part[k] = a + b;
           }
         }
+        s[r] = part[0];
+#pragma unroll
+        for (int k = 1; k < CH; ++k) s[r] += part[k];
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      float s = 0.0f;
 #pragma unroll
-      for (int k = 0; k < CH; ++k)
-        if (lane + 32 * k < nchunks)
+      for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-          for (int e = 0; e < E; ++e) s += v[k][e];
-      const float mean = warp_sum(s) / cols;
-      float q = 0.0f;
+        for (int r = 0; r < R; ++r) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
 #pragma unroll
-      for (int k = 0; k < CH; ++k)
-        if (lane + 32 * k < nchunks)
+      for (int r = 0; r < R; ++r) {
+        mean[r] = s[r] / cols;
+        float part[CH];
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const float d = v[k][e] - mean;
-            q = fmaf(d, d, q);
+        for (int k = 0; k < CH; ++k) {
+          part[k] = 0.0f;
+          if (lane + 32 * k < nchunks) {
+            float a = 0.0f, b = 0.0f;
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+              const float d0 = v[r][k][e] - mean[r], d1 = v[r][k][e + 1] - mean[r];
+              a = fmaf(d0, d0, a);
+              b = fmaf(d1, d1, b);
+            }
+            part[k] = a + b;
           }
-      const float rstd = rsqrtf(warp_sum(q) / cols + eps);
+        }
+        q[r] = part[0];
+#pragma unroll
+        for (int k = 1; k < CH; ++k) q[r] += part[k];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r) q[r] += __shfl_xor_sync(0xffffffffu, q[r], o);
+#pragma unroll
+      for (int r = 0; r < R; ++r) rstd[r] = rsqrtf(q[r] / cols + eps);
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int c = lane + 32 * k;
-        if (c < nchunks) {
-          Vec<TO> o, so;
+        if (c >= nchunks) continue;
+        float gg[E], bb[E];
+        if constexpr (GB_REGS) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            gg[e] = greg[k][e];
+            bb[e] = breg[k][e];
+          }
+        } else {
 #pragma unroll
           for (int e = 0; e < E; e += 4) {
             const uint4 g4 = ld_shared_v4(gb_addr + (c * E + e) * 4);
             const uint4 b4 = ld_shared_v4(gb_addr + (cols + c * E + e) * 4);
-            const float gg[4] = {__uint_as_float(g4.x), __uint_as_float(g4.y), __uint_as_float(g4.z), __uint_as_float(g4.w)};
-            const float bbv[4] = {__uint_as_float(b4.x), __uint_as_float(b4.y), __uint_as_float(b4.z), __uint_as_float(b4.w)};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              o.e[e + u] = OutCvt<TO>::to(fmaf((v[k][e + u] - mean) * rstd, gg[u], bbv[u]));
-              so.e[e + u] = OutCvt<TO>::to(v[k][e + u]);
-            }
+            gg[e] = __uint_as_float(g4.x); gg[e + 1] = __uint_as_float(g4.y);
+            gg[e + 2] = __uint_as_float(g4.z); gg[e + 3] = __uint_as_float(g4.w);
+            bb[e] = __uint_as_float(b4.x); bb[e + 1] = __uint_as_float(b4.y);
+            bb[e + 2] = __uint_as_float(b4.z); bb[e + 3] = __uint_as_float(b4.w);
           }
-          st_stream(yr + c * E, o.u);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!have[r]) continue;
+          const int64_t row = r0 + i0 + r * STREAM_WARPS;
+          Vec<TO> o, so;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            o.e[e] = OutCvt<TO>::to(fmaf((v[r][k][e] - mean[r]) * rstd[r], gg[e], bb[e]));
+            so.e[e] = OutCvt<TO>::to(v[r][k][e]);
+          }
+          st_stream(y + row * cols + c * E, o.u);
           if (sum_out) st_stream(sum_out + row * cols + c * E, so.u);
         }
       }
@@ -415,7 +512,10 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   // complete out of order) and the parity wait passes one phase early.
   const int ns = static_cast<int>(std::min<int64_t>(90, STREAM_SMEM / slot_bytes)) /
                  STREAM_WARPS * STREAM_WARPS;
-  if (ns < STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;
+  // layernorm consumes two rows per warp at a time (rows of <= 1024 16-bit
+  // values): two ring laps of warps
+  const int lanes_rows = MODE == 1 && nchunks <= 128 ? 2 : 1;
+  if (ns < lanes_rows * STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;
   const int smem = ns * slot_bytes + ns * 16 + 128 + (MODE == 1 ? static_cast<int>(cols) * 8 + 16 : 0);
   const TI* xi = reinterpret_cast<const TI*>(x);
   const TI* ri = reinterpret_cast<const TI*>(r);

@@ -24,8 +24,28 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return __fdividef(x, 1.0f + __expf(-2.0f * u));
 }
 
+// erf by Abramowitz & Stegun 7.1.28, erf(x) = 1 - (1 + a1 x + ... + a6 x^6)^-16
+// for x >= 0 (|error| <= 1.6e-6 in fp32, far below the bf16 output ulp and
+// within the fp32 epilogue tolerance): one MUFU reciprocal, no exp, no branch.
+// libdevice erff (~3x the instructions) made the BERT FFN1 epilogue the bound.
+__device__ __forceinline__ float erf_fast(float x) {
+  const float ax = fabsf(x);
+  float p = fmaf(0.0000430638f, ax, 0.0002765672f);
+  p = fmaf(p, ax, 0.0001520143f);
+  p = fmaf(p, ax, 0.0092705272f);
+  p = fmaf(p, ax, 0.0422820123f);
+  p = fmaf(p, ax, 0.0705230784f);
+  p = fmaf(p, ax, 1.0f);
+  float r = __fdividef(1.0f, p);  // p >= 1; overflow -> r = 0 -> erf = 1
+  r *= r;
+  r *= r;
+  r *= r;
+  r *= r;
+  return copysignf(1.0f - r, x);
+}
+
 __device__ __forceinline__ float gelu_erf(float x) {
-  return 0.5f * x * (1.0f + erff(x * 0.7071067811865476f));
+  return 0.5f * x * (1.0f + erf_fast(x * 0.7071067811865476f));
 }
 
 template <int EPI>

@@ -572,14 +572,17 @@ int make_store_map(CUtensorMap* map, void* C, afg_dtype c, int64_t M, int64_t N,
   return 1;
 }
 
-// CTA-pair tiles (256 x 256) for BLOCK_N = 256 problems with at least one
-// full wave of pair tiles; AFG_GEMM_PAIR=0 disables them (A/B measurements).
-bool use_pair_tiles(int block_n, int64_t M, int64_t N) {
+// CTA-pair tiles (256 x 256) for BLOCK_N = 256 problems with K >= 768 and at
+// least one full wave of pair tiles; AFG_GEMM_PAIR=0 disables them (A/B).
+bool use_pair_tiles(int block_n, int64_t M, int64_t N, int64_t K) {
   static const bool enabled = [] {
     const char* e = getenv("AFG_GEMM_PAIR");
     return !(e && atoi(e) == 0);
   }();
-  if (!enabled || block_n != 256 || M < 256) return false;
+  // short K (<= 8 k-blocks) is epilogue / HBM bound: the pair's cross-CTA
+  // accumulator hand-off costs more than the halved B staging saves
+  // (measured: ResNet 1x1 convs and BERT K = 768 GEMMs)
+  if (!enabled || block_n != 256 || M < 256 || K < 768) return false;
   const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
   return pair_tiles >= num_sms() / 2;
 }
@@ -595,7 +598,7 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   // BLOCK_N: 256 when N is large enough to fill it, else 128 / 64.
   const int block_n = N >= 256 ? 256 : (N > 64 ? 128 : 64);
   // 256 x 256 tiles on a CTA pair when there are enough of them to fill the GPU
-  const bool pair = use_pair_tiles(block_n, M, N);
+  const bool pair = use_pair_tiles(block_n, M, N, K);
   const CUtensorMapDataType tdt =
       ab == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmA, tmB;
