@@ -12,6 +12,7 @@
 #include <cuda_fp16.h>
 
 #include "../../include/afg.h"
+#include "sm100.cuh"
 
 namespace afg {
 
@@ -53,6 +54,63 @@ __device__ __forceinline__ float apply_act(float v) {
   if constexpr (EPI == AFG_EPI_BIAS_RELU) return fmaxf(v, 0.0f);
   if constexpr (EPI == AFG_EPI_BIAS_GELU_TANH) return gelu_tanh(v);
   if constexpr (EPI == AFG_EPI_BIAS_GELU_ERF) return gelu_erf(v);
+  return v;
+}
+
+// Packed (f32x2) activations for a pair of accumulator values: the same
+// formulas as above with the FMA-pipe work in one issue slot per pair -- the
+// GEMM epilogue of a short-K GEMM (BERT FFN1, K = 768) is issue-bound.
+__device__ __forceinline__ uint64_t gelu_tanh2(uint64_t x) {
+  using namespace sm100;
+  const uint64_t x2 = fmul2(x, x);
+  const uint64_t t = ffma2(x2, f2(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f),
+                           f2(0.7978845608028654f, 0.7978845608028654f));
+  // e = exp(-2u) = 2^(-2 log2(e) u)
+  const uint64_t z = fmul2(fmul2(t, x), f2(-2.8853900817779268f, -2.8853900817779268f));
+  float z0, z1, x0, x1;
+  f2split(z, z0, z1);
+  f2split(x, x0, x1);
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(z0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(z1));
+  return f2(__fdividef(x0, 1.0f + e0), __fdividef(x1, 1.0f + e1));
+}
+
+__device__ __forceinline__ uint64_t gelu_erf2(uint64_t x) {
+  using namespace sm100;
+  float x0, x1;
+  f2split(x, x0, x1);
+  // |x| / sqrt(2) for both lanes, then A&S 7.1.28 in packed Horner form
+  const uint64_t a = fmul2(f2(fabsf(x0), fabsf(x1)), f2(0.7071067811865476f, 0.7071067811865476f));
+  uint64_t p = ffma2(f2(0.0000430638f, 0.0000430638f), a, f2(0.0002765672f, 0.0002765672f));
+  p = ffma2(p, a, f2(0.0001520143f, 0.0001520143f));
+  p = ffma2(p, a, f2(0.0092705272f, 0.0092705272f));
+  p = ffma2(p, a, f2(0.0422820123f, 0.0422820123f));
+  p = ffma2(p, a, f2(0.0705230784f, 0.0705230784f));
+  p = ffma2(p, a, f2(1.0f, 1.0f));
+  float p0, p1;
+  f2split(p, p0, p1);
+  uint64_t r = f2(__fdividef(1.0f, p0), __fdividef(1.0f, p1));
+  r = fmul2(r, r);
+  r = fmul2(r, r);
+  r = fmul2(r, r);
+  r = fmul2(r, r);  // (1 + ...)^-16 = 1 - erf(|x| / sqrt 2)
+  float r0, r1;
+  f2split(r, r0, r1);
+  // 0.5 x (1 + erf) with erf carrying the sign of x
+  const uint64_t one_p_erf = f2(x0 >= 0.0f ? 2.0f - r0 : r0, x1 >= 0.0f ? 2.0f - r1 : r1);
+  return fmul2(fmul2(x, f2(0.5f, 0.5f)), one_p_erf);
+}
+
+template <int EPI>
+__device__ __forceinline__ uint64_t apply_act2(uint64_t v) {
+  if constexpr (EPI == AFG_EPI_BIAS_GELU_TANH) return gelu_tanh2(v);
+  if constexpr (EPI == AFG_EPI_BIAS_GELU_ERF) return gelu_erf2(v);
+  if constexpr (EPI == AFG_EPI_BIAS_RELU) {
+    float a, b;
+    sm100::f2split(v, a, b);
+    return sm100::f2(fmaxf(a, 0.0f), fmaxf(b, 0.0f));
+  }
   return v;
 }
 

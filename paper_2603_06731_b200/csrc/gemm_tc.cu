@@ -148,22 +148,25 @@ __device__ __forceinline__ void epi_values32(const uint32_t (&acc)[32], const Ge
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]);
   if constexpr (EPI != AFG_EPI_NONE) {
     if (col0 + 32 <= a.N) {
+      // bias add and activation on f32x2 pairs (one issue slot per pair)
       const float4* b4 = reinterpret_cast<const float4*>(a.bias + col0);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float4 b = __ldg(b4 + j);
-        v[4 * j + 0] += b.x;
-        v[4 * j + 1] += b.y;
-        v[4 * j + 2] += b.z;
-        v[4 * j + 3] += b.w;
+        uint64_t p0 = fadd2(f2(v[4 * j], v[4 * j + 1]), f2(b.x, b.y));
+        uint64_t p1 = fadd2(f2(v[4 * j + 2], v[4 * j + 3]), f2(b.z, b.w));
+        p0 = apply_act2<EPI>(p0);
+        p1 = apply_act2<EPI>(p1);
+        f2split(p0, v[4 * j], v[4 * j + 1]);
+        f2split(p1, v[4 * j + 2], v[4 * j + 3]);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (col0 + j < a.N) v[j] += __ldg(a.bias + col0 + j);
-    }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = apply_act<EPI>(v[j]);
+      for (int j = 0; j < 32; ++j) v[j] = apply_act<EPI>(v[j]);
+    }
   }
   if (a.residual != nullptr && row < a.M) {
     const OutT* rrow = reinterpret_cast<const OutT*>(a.residual) + static_cast<int64_t>(row) * a.ldc + col0;
@@ -623,7 +626,11 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   args.num_n_blocks = static_cast<int>((N + block_n - 1) / block_n);
   args.epi = static_cast<int>(epi);
   CUtensorMap tmC;
-  args.tma_store = make_store_map(&tmC, C, c, M, N, ldc);
+  static const bool no_tma_store = [] {
+    const char* e = getenv("AFG_GEMM_TMA_STORE");
+    return e && atoi(e) == 0;
+  }();
+  args.tma_store = no_tma_store ? 0 : make_store_map(&tmC, C, c, M, N, ldc);
   cudaError_t e;
   if (pair)
     e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
