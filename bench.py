@@ -152,10 +152,9 @@ from paper_2603_06731_b200.shard import shard_rows, shard_seed  # noqa: E402
 class GemmBF16:
     """BASELINE configs[1]: bf16 C = gelu_tanh(A B + bias), fp32 accumulate."""
 
-    name = "gemm_bf16_gelu"
-
     def __init__(self, size):
         self.n = size
+        self.name = f"gemm_bf16_gelu_{size}"  # per-size traffic entry in profiles/traffic.json
 
     def config(self, world):
         return {"workload": f"bf16 matmul {self.n}x{self.n}x{self.n} + bias + tanh-GELU "

@@ -38,7 +38,7 @@ using namespace sm100;
 
 constexpr int BLOCK_M = 128;
 constexpr int BLOCK_K = 64;  // 64 x 16-bit = one 128-byte swizzle row
-constexpr int GROUP_M = 16;  // tile raster: 16 M-blocks share B tiles in L2
+constexpr int GROUP_M = 16;  // default tile raster: 16 M-blocks share B tiles in L2
 
 struct GemmTcArgs {
   int M, N, K;
@@ -47,6 +47,7 @@ struct GemmTcArgs {
   const void* residual;
   void* C;
   int num_m_blocks, num_n_blocks;
+  int group_m;  // tile raster: M-blocks per group (consecutive tiles walk M first)
   int epi;
   int tma_store;  // 1: stage C through swizzled smem + TMA bulk tensor store
   // implicit-GEMM conv (IM2COL): output pixel m = (n, p, q) over OH x OW,
@@ -70,11 +71,12 @@ struct SmemLayout {
   static constexpr int TOTAL = BAR_OFFSET + NUM_BARS * 8 + 16 + 1024;  // +1024 align slack
 };
 
-__device__ __forceinline__ void tile_coords(int t, int nmb, int nnb, int& mb, int& nb) {
-  const int per_group = GROUP_M * nnb;
+__device__ __forceinline__ void tile_coords(int t, int nmb, int nnb, int group_m, int& mb,
+                                            int& nb) {
+  const int per_group = group_m * nnb;
   const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsize = min(nmb - first_m, GROUP_M);
+  const int first_m = group * group_m;
+  const int gsize = min(nmb - first_m, group_m);
   const int r = t - group * per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t phase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
         int mb, nb;
-        tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
         const int m0 = mb * TILE_M + static_cast<int>(rank) * BLOCK_M;
         const int n0 = nb * BLOCK_N + static_cast<int>(rank) * L::B_ROWS;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(384, 1)
       const bool leader = ew == 0 && lane == 0;
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
-        tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
         const int acc = iter & 1;
         mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
         tc_fence_after();
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(384, 1)
     } else {
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
-        tile_coords(t, args.num_m_blocks, args.num_n_blocks, mb, nb);
+        tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
         const int acc = iter & 1;
         const uint32_t acc_par = (iter >> 1) & 1;
         mbar_wait(&tfull_bar[acc], acc_par);
@@ -623,6 +625,12 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   args.C = C;
   const int tile_m = pair ? 2 * BLOCK_M : BLOCK_M;
   args.num_m_blocks = static_cast<int>((M + tile_m - 1) / tile_m);
+  // raster groups span 2048 rows of A (16 x 128 or 8 x 256-row pair tiles)
+  static const int group_env = [] {
+    const char* e = getenv("AFG_GEMM_GROUP_M");
+    return e ? atoi(e) : 0;
+  }();
+  args.group_m = group_env > 0 ? group_env : (pair ? GROUP_M / 2 : GROUP_M);
   args.num_n_blocks = static_cast<int>((N + block_n - 1) / block_n);
   args.epi = static_cast<int>(epi);
   CUtensorMap tmC;
@@ -685,6 +693,7 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   args.C = y;
   args.num_m_blocks = static_cast<int>((M + BLOCK_M - 1) / BLOCK_M);
   args.num_n_blocks = static_cast<int>((OC + block_n - 1) / block_n);
+  args.group_m = GROUP_M;
   args.epi = static_cast<int>(epi);
   args.c_blocks = static_cast<int>(C / BLOCK_K);
   args.KW = static_cast<int>(KW);
