@@ -44,6 +44,7 @@ constexpr int BN = 128;  // keys per KV tile
 // (+4% at D = 128); 3/8 and above spill and lose 10%.
 constexpr unsigned POLY_PAIRS = 0x12;
 
+
 struct AttnArgs {
   const float* bias;  // [BH, Nq, Nk] or null
   void* o;
@@ -61,13 +62,19 @@ struct AttnSmem {
   static constexpr int TILE = BM * D * 2;  // one Q / K / V tile (BM == BN rows)
   // K and V tiles share one ring (K(j), V(j), K(j+1), ...): 5 x 32 KB at D=128
   // keeps 2.5 KV tiles in flight next to the two resident Q tiles.
-  static constexpr int STAGES = D == 64 ? 10 : 5;
+  // Q buffers: with two, the next unit's Q tiles load while the current unit
+  // runs. Measured: +3% at D = 64 (BERT, 4-tile units); at D = 128 the two
+  // K/V stages it would cost matter more (-1%), so one buffer there.
+  static constexpr int QBUF = D == 64 ? 2 : 1;
+  static constexpr int STAGES = D == 64 ? (QBUF == 2 ? 8 : 10) : (QBUF == 2 ? 3 : 5);
   static constexpr int QA_OFF = 0;
   static constexpr int QB_OFF = TILE;
-  static constexpr int RING_OFF = 2 * TILE;
+  static constexpr int QBUF_BYTES = 2 * TILE;
+  static constexpr int RING_OFF = QBUF * QBUF_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * TILE;
-  // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2][2], o_full[2], o_empty[2]
-  static constexpr int NUM_BARS = 2 + 2 * STAGES + 10;
+  // q_full[QBUF], q_empty[QBUF], kv_full[S], kv_empty[S], s_full[2], p_full[2][2],
+  // o_full[2], o_empty[2]
+  static constexpr int NUM_BARS = 2 * QBUF + 2 * STAGES + 10;
   static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
   static_assert(TOTAL <= 232448, "attention smem over the 227 KB opt-in limit");
 };
@@ -146,9 +153,10 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;
+  constexpr int QBUF = L::QBUF;
+  uint64_t* q_full = bars;            // [QBUF]
+  uint64_t* q_empty = bars + QBUF;    // [QBUF]
+  uint64_t* kv_full = bars + 2 * QBUF;
   uint64_t* kv_empty = kv_full + NS;
   uint64_t* s_full = kv_empty + NS;  // [2]
   uint64_t* p_full = s_full + 2;     // [tile][half]: P columns of keys [0,64) / [64,128)
@@ -197,8 +205,10 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int b = 0; b < QBUF; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1);
+    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -419,11 +429,14 @@ __global__ void __launch_bounds__(384, 1)
           const int lin = unit_of(u);
           if (lin >= n_units) break;
           const Unit w = decode(lin);
-          mbar_wait(q_empty, (u & 1) ^ 1);  // the previous unit's S MMAs are done with Q
-          mbar_arrive_expect_tx(q_full, 2 * L::TILE);
+          const int qb = u % QBUF;
+          // the S MMAs of the unit that last used this Q buffer are done
+          mbar_wait(&q_empty[qb], ((u / QBUF) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qb], 2 * L::TILE);
           for (int g = 0; g < 2; ++g)
             for (int a = 0; a < DB; ++a)
-              tma_load_4d(smem + (g ? L::QB_OFF : L::QA_OFF) + a * (BM * 128), &tmQ, q_full,
+              tma_load_4d(smem + qb * L::QBUF_BYTES + (g ? L::QB_OFF : L::QA_OFF) + a * (BM * 128),
+                          &tmQ, &q_full[qb],
                           a * 64, w.q0 + g * BM, w.hh, w.bb);
           const int items = 2 * max(w.nkv0, w.nkv1);
           for (int it = 0; it < items; ++it, ++n) {
@@ -457,8 +470,10 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&kv_full[n % NS], (n / NS) & 1);
         tc_fence_after();
       };
+      int qb = 0;  // Q buffer of the current unit
       auto issue_s = [&](int g, int j) {
-        const uint64_t qd = q_desc0 + (g ? QB_STEP : 0);
+        const uint64_t qd =
+            q_desc0 + (g ? QB_STEP : 0) + static_cast<uint64_t>(qb) * (L::QBUF_BYTES >> 4);
         const uint64_t kd = k_desc0 + static_cast<uint64_t>((nb + 2 * j) % NS) * SLOT_STEP;
         if (args.dbg != 2) {
 #pragma unroll
@@ -487,11 +502,12 @@ __global__ void __launch_bounds__(384, 1)
         if (lin >= n_units) break;
         const Unit w = decode(lin);
         const int nkv_max = max(w.nkv0, w.nkv1);
-        mbar_wait(q_full, u & 1);
+        qb = u % QBUF;
+        mbar_wait(&q_full[qb], (u / QBUF) & 1);
         wait_item(nb);
         if (w.nkv0 > 0) issue_s(0, 0);
         if (w.nkv1 > 0) issue_s(1, 0);
-        if (nkv_max <= 1) mma_commit_if(leader, q_empty);  // last S of the unit issued
+        if (nkv_max <= 1) mma_commit_if(leader, &q_empty[qb]);  // last S of the unit issued
         mma_commit_if(leader, &kv_empty[nb % NS]);
         for (int j = 0; j < nkv_max; ++j) {
           const int jn = j + 1;
@@ -521,7 +537,7 @@ __global__ void __launch_bounds__(384, 1)
               }
             }
           }
-          if (jn == nkv_max - 1) mma_commit_if(leader, q_empty);  // last S of the unit issued
+          if (jn == nkv_max - 1) mma_commit_if(leader, &q_empty[qb]);  // last S of the unit issued
           mma_commit_if(leader, &kv_empty[(nb + 2 * j + 1) % NS]);
           if (k_next_ready) mma_commit_if(leader, &kv_empty[(nb + 2 * jn) % NS]);
         }
