@@ -51,6 +51,9 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
                    afg_dtype ab, afg_dtype c, afg_layout b_layout, afg_epilogue epi,
                    cudaStream_t stream);
 
+afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, int64_t B,
+                     int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_epilogue epi,
+                     cudaStream_t stream);
 afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int64_t B,
                    int64_t H, int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
                    int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh, int64_t dw,

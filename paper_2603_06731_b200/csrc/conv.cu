@@ -155,6 +155,12 @@ afg_status afg_conv2d_nhwc(const void* x, const void* w, const float* bias, void
     // 1x1 / stride 1: the implicit GEMM is the plain GEMM on [B*H*W, C] x [OC, C]^T
     return gemm_tc(x, C, w, C, bias, nullptr, y, OC, M, OC, C, dt, dt, AFG_B_NK, epi, s);
   }
+  if (tc && KH == 3 && KW == 3 && sh == 1 && sw == 1 && dh == 1 && dw == 1 && pt == 1 &&
+      pl == 1 && OH == H && OW == W) {
+    // 3x3 / stride 1 / pad 1: the input halo is staged once per tile, not per tap
+    st = conv_halo(x, w, bias, y, B, H, W, C, OC, dt, epi, s);
+    if (st != AFG_ERR_UNSUPPORTED) return st;
+  }
   if (tc && sh <= 8 && sw <= 8) {
     st = conv_tc(x, w, bias, y, B, H, W, C, OC, KH, KW, sh, sw, pt, pl, dh, dw, OH, OW, dt, epi,
                  s);

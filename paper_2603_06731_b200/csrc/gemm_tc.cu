@@ -501,6 +501,199 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ------------------------------------------------- halo-tiled 3x3 conv (K2b) --
+// 3x3 / stride 1 / pad 1 convolution (every stride-1 3x3 layer of ResNet-50)
+// with the input staged ONCE per 64-channel chunk and tile instead of once per
+// filter tap: a tile = R output rows x P output columns (P = power of two >=
+// W + 2, R = 128 / P, so M = 128 pixels per tile, columns >= W discarded). One
+// 4-D TMA tile load brings the (R + 2) x P halo of input pixels (columns from
+// -1, rows from oy0 - 1; out-of-bounds rows / columns are zero-filled by the
+// TMA unit = the conv padding) into 128B-swizzled smem with a row pitch of P
+// pixels. Tap (ky, kx) is then the same buffer read at a pixel offset
+// ky * P + kx: the UMMA descriptor start moves by (ky P + kx) 128-byte rows.
+// The 128B swizzle is a function of the absolute smem address for both the TMA
+// write and the MMA read, so starts that are not 1024-byte aligned need no
+// base-offset correction (verified on B200: setting it to kx breaks parity).
+// L2 -> smem traffic per tile drops 9 x 16 KB -> (R+2) P 128 B (4.5x at W=56)
+// relative to the im2col loader, which bound the 56x56 layers.
+struct HaloArgs {
+  GemmTcArgs g;            // epilogue: M (output pixels), N = OC, ldc, bias, C, epi
+  int H, W, C;             // input (= output) extent, channels
+  int P, R;                // halo row pitch (pixels), output rows per tile
+  int tiles_per_img, num_m_tiles, c_chunks;
+};
+
+template <int BLOCK_N>
+struct HaloSmem {
+  static constexpr int A_BYTES = (128 + 2 * 64) * 128;  // (R+2) x P pixels at P = 64
+  static constexpr int B_STAGES = BLOCK_N == 64 ? 8 : (BLOCK_N == 128 ? 6 : 4);
+  static constexpr int B_BYTES = BLOCK_N * 128;  // BLOCK_N rows x 64 channels (one tap)
+  static constexpr int B_OFF = 2 * A_BYTES;
+  static constexpr int BAR_OFF = B_OFF + B_STAGES * B_BYTES;
+  // a_full[2], a_empty[2], b_full[S], b_empty[S], tfull[2], tempty[2]
+  static constexpr int NUM_BARS = 4 + 2 * B_STAGES + 4;
+  static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
+  static_assert(TOTAL <= 232448, "halo conv smem over the 227 KB opt-in limit");
+};
+
+template <int BLOCK_N, bool AB_BF16, typename OutT>
+__global__ void __launch_bounds__(384, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmW, const HaloArgs args) {
+  using L = HaloSmem<BLOCK_N>;
+  constexpr int NS = L::B_STAGES;
+  constexpr uint32_t TMEM_COLS = 2 * BLOCK_N <= 128 ? 128 : (2 * BLOCK_N <= 256 ? 256 : 512);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = bars + 2;
+  uint64_t* b_full = bars + 4;
+  uint64_t* b_empty = b_full + NS;
+  uint64_t* tfull = b_empty + NS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nnb = args.g.num_n_blocks;
+  const int num_tiles = args.num_m_tiles * nnb;
+  const int a_bytes = (args.R + 2) * args.P * 128;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // tile t: output-pixel block mt (image n, rows oy0..oy0+R-1), OC block nb
+  // (nb fastest: consecutive tiles reuse the same halo in L2)
+  auto coords = [&](int t, int& n, int& oy0, int& nb) {
+    const int mt = t / nnb;
+    nb = t - mt * nnb;
+    n = mt / args.tiles_per_img;
+    oy0 = (mt - n * args.tiles_per_img) * args.R;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    if (lane == 0) {
+      int ai = 0, bs = 0;
+      uint32_t bph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int n, oy0, nb;
+        coords(t, n, oy0, nb);
+        for (int cb = 0; cb < args.c_chunks; ++cb, ++ai) {
+          const int slot = ai & 1;
+          mbar_wait(&a_empty[slot], ((ai >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(a_bytes));
+          tma_load_4d(smem + slot * L::A_BYTES, &tmX, &a_full[slot], cb * 64, -1, oy0 - 1, n);
+          for (int tap = 0; tap < 9; ++tap) {
+            mbar_wait(&b_empty[bs], bph ^ 1);
+            mbar_arrive_expect_tx(&b_full[bs], L::B_BYTES);
+            tma_load_2d(smem + L::B_OFF + bs * L::B_BYTES, &tmW, &b_full[bs],
+                        tap * args.C + cb * 64, nb * BLOCK_N);
+            if (++bs == NS) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------- MMA issuer (warp-uniform)
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_f16(BLOCK_M, BLOCK_N, AB_BF16 ? 1u : 0u, 0u, 0u);
+    const uint64_t a_desc0 = desc_kmajor_sw128(smem_u32(smem));
+    const uint64_t b_desc0 = desc_kmajor_sw128(smem_u32(smem + L::B_OFF));
+    int ai = 0, bs = 0, iter = 0;
+    uint32_t bph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      const int acc = iter & 1;
+      mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+      for (int cb = 0; cb < args.c_chunks; ++cb, ++ai) {
+        const int slot = ai & 1;
+        mbar_wait(&a_full[slot], (ai >> 1) & 1);
+        tc_fence_after();
+        const uint64_t a_slot = a_desc0 + static_cast<uint64_t>(slot) * (L::A_BYTES >> 4);
+        for (int tap = 0; tap < 9; ++tap) {
+          const int ky = tap / 3, kx = tap - 3 * (tap / 3);
+          mbar_wait(&b_full[bs], bph);
+          tc_fence_after();
+          // tap window: (ky * P + kx) 128-byte pixel rows into the halo
+          const uint64_t ad = a_slot + static_cast<uint64_t>((ky * args.P + kx) * 8);
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(bs) * (L::B_BYTES >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_f16_ss_if(leader, d_tmem, ad + static_cast<uint64_t>(k * 2), bd + static_cast<uint64_t>(k * 2),
+                          idesc, (cb | tap | k) != 0 ? 1u : 0u);
+          mma_commit_if(leader, &b_empty[bs]);
+          if (++bs == NS) {
+            bs = 0;
+            bph ^= 1;
+          }
+        }
+        mma_commit_if(leader, &a_empty[slot]);
+      }
+      mma_commit_if(leader, &tfull[acc]);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue --
+    // accumulator row m = r * P + c -> output pixel (n, oy0 + r, c) if c < W
+    const int eg = (warp - 4) / 4;
+    const int ew = warp % 4;
+    const int m = ew * 32 + lane;
+    const int r = m / args.P, c = m - r * args.P;
+    int iter = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      int n, oy0, nb;
+      coords(t, n, oy0, nb);
+      const int acc = iter & 1;
+      mbar_wait(&tfull[acc], (iter >> 1) & 1);
+      tc_fence_after();
+      const int oy = oy0 + r;
+      const int out_row = (c < args.W && oy < args.H) ? (n * args.H + oy) * args.W + c : args.g.M;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
+#pragma unroll 1
+      for (int ch = eg; ch < BLOCK_N / 32; ch += 2) {
+        uint32_t v[32];
+        tmem_ld32(t_row + ch * 32, v);
+        tmem_wait_ld();
+        if (ch + 2 >= BLOCK_N / 32) {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        const int col0 = nb * BLOCK_N + ch * 32;
+        if (col0 < args.g.N) store_chunk32_rt<OutT>(v, args.g, out_row, col0);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
 // --------------------------------------------------------------- host side --
 
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT,
@@ -720,6 +913,76 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
     e = AFG_CONV_V(64, 8);
 #undef AFG_CONV_V
   return cuda_status(e, "conv_tc launch");
+}
+
+
+// Halo-tiled 3x3 / stride-1 / pad-1 conv (see conv_halo_kernel). Returns
+// AFG_ERR_UNSUPPORTED when the shape does not fit (the caller then uses the
+// im2col path).
+afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, int64_t B,
+                     int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_epilogue epi,
+                     cudaStream_t stream) {
+  static const int mode = [] {  // AFG_CONV_HALO=0 turns it off (A/B measurements)
+    const char* e = getenv("AFG_CONV_HALO");
+    return e ? atoi(e) : 1;
+  }();
+  // W < 20 (P = 16) wastes 2 of every 16 columns and, at 14x14, 2 of 16 rows
+  // too: measured slower than the im2col loader there (60 vs 55 us)
+  if (mode == 0 || C % 64 != 0 || W < 20 || W + 2 > 64 || (dt != AFG_BF16 && dt != AFG_F16))
+    return AFG_ERR_UNSUPPORTED;
+  const int P = W + 2 <= 16 ? 16 : (W + 2 <= 32 ? 32 : 64);
+  const int R = 128 / P;
+  const int block_n = OC >= 256 ? 256 : (OC > 64 ? 128 : 64);
+  const CUtensorMapDataType tdt =
+      dt == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tmX, tmW;
+  const uint64_t dims[4] = {static_cast<uint64_t>(C), static_cast<uint64_t>(W),
+                            static_cast<uint64_t>(H), static_cast<uint64_t>(B)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(C) * 2, static_cast<uint64_t>(W * C) * 2,
+                               static_cast<uint64_t>(H * W * C) * 2};
+  const uint32_t box[4] = {64, static_cast<uint32_t>(P), static_cast<uint32_t>(R + 2), 1};
+  afg_status st = make_tmap(&tmX, x, tdt, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != AFG_OK) return st;
+  st = make_tmap_2d(&tmW, w, tdt, 2, 9 * C, OC, 9 * C, 64, block_n);
+  if (st != AFG_OK) return st;
+  HaloArgs a{};
+  a.g.M = static_cast<int>(B * H * W);
+  a.g.N = static_cast<int>(OC);
+  a.g.K = static_cast<int>(9 * C);
+  a.g.ldc = static_cast<int>(OC);
+  a.g.bias = bias;
+  a.g.residual = nullptr;
+  a.g.C = y;
+  a.g.num_n_blocks = static_cast<int>((OC + block_n - 1) / block_n);
+  a.g.epi = static_cast<int>(epi);
+  a.H = static_cast<int>(H);
+  a.W = static_cast<int>(W);
+  a.C = static_cast<int>(C);
+  a.P = P;
+  a.R = R;
+  a.tiles_per_img = static_cast<int>((H + R - 1) / R);
+  a.num_m_tiles = static_cast<int>(B) * a.tiles_per_img;
+  a.c_chunks = static_cast<int>(C / 64);
+  const int tiles = a.num_m_tiles * a.g.num_n_blocks;
+  const int grid = std::min(tiles, num_sms());
+  auto go = [&](auto kern, int smem) {
+    static bool configured = false;
+    (void)configured;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 384, smem, stream>>>(tmX, tmW, a);
+    count_launch();
+    return cudaGetLastError();
+  };
+  cudaError_t e;
+#define AFG_HALO(BN)                                                                         \
+  (dt == AFG_BF16 ? go(conv_halo_kernel<BN, true, __nv_bfloat16>, HaloSmem<BN>::TOTAL)      \
+                  : go(conv_halo_kernel<BN, false, __half>, HaloSmem<BN>::TOTAL))
+  if (block_n == 256) e = AFG_HALO(256);
+  else if (block_n == 128) e = AFG_HALO(128);
+  else e = AFG_HALO(64);
+#undef AFG_HALO
+  return cuda_status(e, "conv_halo launch");
 }
 
 }  // namespace afg

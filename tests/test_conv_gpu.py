@@ -48,6 +48,23 @@ def test_implicit_gemm_tc(cuda, B, H, W, C, OC, k, s, p):
     conv_case(B, H, W, C, OC, k, s, p)
 
 
+# 3x3 / stride 1 / pad 1 with 20 <= W <= 62 runs the halo-tiled kernel (input
+# staged once per tile and channel chunk, taps as shifted smem windows): both
+# halo pitches (P = 32 / 64), rows past the image bottom (H % R != 0), ragged
+# OC, several channel chunks, fp16, no epilogue; narrower images (the im2col
+# path) alongside.
+@pytest.mark.parametrize("B,H,W,C,OC,dt,epi", [
+    (2, 56, 56, 64, 64, torch.bfloat16, Epilogue.BIAS_RELU),
+    (2, 28, 28, 128, 128, torch.bfloat16, Epilogue.BIAS_RELU),
+    (2, 14, 14, 256, 256, torch.bfloat16, Epilogue.BIAS_RELU),
+    (3, 23, 21, 64, 96, torch.float16, Epilogue.BIAS),
+    (1, 31, 62, 192, 64, torch.bfloat16, Epilogue.NONE),
+    (2, 57, 40, 128, 320, torch.bfloat16, Epilogue.BIAS_RELU),
+])
+def test_halo_conv_3x3(cuda, B, H, W, C, OC, dt, epi):
+    conv_case(B, H, W, C, OC, 3, 1, 1, dt=dt, epi=epi)
+
+
 def test_implicit_gemm_dilation_and_no_epilogue(cuda):
     conv_case(2, 12, 12, 64, 64, 3, 1, 2, dil=2, epi=Epilogue.NONE)
 
