@@ -64,8 +64,11 @@ struct SmemLayout {
   static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 2;
   static constexpr int B_BYTES = B_ROWS * BLOCK_K * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;  // 2 x (128 rows x 128 B) C staging
-  static constexpr int EPI_BYTES = 2 * BLOCK_M * 128;
+  // C staging: 2 epilogue groups x EPI_BUFS x (128 rows x 128 B); two buffers
+  // per group when they fit next to the operand stages
+  static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int EPI_BUFS = EPI_OFFSET + 4 * BLOCK_M * 128 + 2048 <= 232448 ? 2 : 1;
+  static constexpr int EPI_BYTES = 2 * EPI_BUFS * BLOCK_M * 128;
   static constexpr int BAR_OFFSET = EPI_OFFSET + EPI_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TOTAL = BAR_OFFSET + NUM_BARS * 8 + 16 + 1024;  // +1024 align slack
@@ -407,10 +410,13 @@ __global__ void __launch_bounds__(384, 1)
       }
     };
     if (args.tma_store) {
-      // C chunk of 128 rows x 128 B staged in 128B-swizzled smem (one buffer
-      // per group), then one TMA bulk tensor store by the group leader.
+      // C chunk of 128 rows x 128 B staged in 128B-swizzled smem (with two
+      // buffers per group a chunk is written while the previous chunk's TMA
+      // store still reads its buffer), then one TMA bulk tensor store by the
+      // group leader.
       constexpr int CW = 128 / static_cast<int>(sizeof(OutT));  // columns per chunk
-      uint8_t* stage = smem + L::EPI_OFFSET + eg * (BLOCK_M * 128);
+      uint8_t* stage_base = smem + L::EPI_OFFSET + eg * L::EPI_BUFS * (BLOCK_M * 128);
+      int staged = 0;  // chunks this group has staged (buffer = staged & 1)
       const bool leader = ew == 0 && lane == 0;
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
@@ -421,15 +427,16 @@ __global__ void __launch_bounds__(384, 1)
         const int m0 = mb * TILE_M + static_cast<int>(rank) * BLOCK_M;
         const int row = m0 + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
-        const uint32_t srow = smem_u32(stage + rloc * 128);
         constexpr int NCH = BLOCK_N / CW;
         if (eg >= NCH) release_acc(acc);  // no chunk for this group: still release once
 #pragma unroll 1
         for (int cc = eg; cc < NCH; cc += 2) {
           const int n0 = nb * BLOCK_N + cc * CW;
           const bool live = n0 < args.N;  // uniform across the group
+          uint8_t* stage = stage_base + (staged % L::EPI_BUFS) * (BLOCK_M * 128);
+          const uint32_t srow = smem_u32(stage + rloc * 128);
           if (live) {
-            if (leader) tma_store_wait_read<0>();
+            if (leader) tma_store_wait_read<L::EPI_BUFS - 1>();  // last store from this buffer
             epi_bar_sync(eg);
           }
 #pragma unroll
@@ -465,6 +472,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_store_2d(&tmC, stage, n0, m0);
             tma_store_commit();
           }
+          ++staged;
         }
       }
       if (leader) tma_store_wait<0>();
@@ -833,14 +841,16 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   }();
   args.tma_store = no_tma_store ? 0 : make_store_map(&tmC, C, c, M, N, ldc);
   cudaError_t e;
-  if (pair)
+  if (pair && K >= 2048)  // long K: operand stages first (6 x 32 KB, one C buffer per group)
     e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+  else if (pair)  // shorter K: the epilogue matters more (5 stages, two C buffers per group)
+    e = dispatch_types<256, 5, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 256)
-    e = dispatch_types<256, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+    e = dispatch_types<256, 3>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 128)
-    e = dispatch_types<128, 6>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+    e = dispatch_types<128, 5>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else
-    e = dispatch_types<64, 8>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+    e = dispatch_types<64, 6>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   if (e == cudaErrorNotSupported)
     return set_error(AFG_ERR_UNSUPPORTED, "gemm_tc: unsupported (ab, c) dtype pair");
   return cuda_status(e, "gemm_tc launch");
@@ -906,11 +916,11 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
        ? launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, tmC, args, stream) \
        : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, tmC, args, stream))
   if (block_n == 256)
-    e = AFG_CONV_V(256, 4);
+    e = AFG_CONV_V(256, 3);
   else if (block_n == 128)
-    e = AFG_CONV_V(128, 6);
+    e = AFG_CONV_V(128, 5);
   else
-    e = AFG_CONV_V(64, 8);
+    e = AFG_CONV_V(64, 6);
 #undef AFG_CONV_V
   return cuda_status(e, "conv_tc launch");
 }
