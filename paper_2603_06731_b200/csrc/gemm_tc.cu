@@ -439,15 +439,17 @@ __global__ void __launch_bounds__(384, 1)
             if (leader) tma_store_wait_read<L::EPI_BUFS - 1>();  // last store from this buffer
             epi_bar_sync(eg);
           }
+          // the chunk's TMEM columns in one round trip (all loads, one wait)
+          uint32_t rr[CW / 32][32];
+#pragma unroll
+          for (int h = 0; h < CW / 32; ++h) tmem_ld32(t_row + cc * CW + h * 32, rr[h]);
+          tmem_wait_ld();
+          if (cc + 2 >= NCH) release_acc(acc);  // last TMEM read of the tile
 #pragma unroll
           for (int h = 0; h < CW / 32; ++h) {
-            uint32_t r[32];
-            tmem_ld32(t_row + cc * CW + h * 32, r);
-            tmem_wait_ld();
-            if (h == CW / 32 - 1 && cc + 2 >= NCH) release_acc(acc);  // last TMEM read of the tile
             if (!live) continue;
             float v[32];
-            epi_values32_rt<OutT>(r, args, row, n0 + h * 32, v);
+            epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v);
             // 32 values -> 64 B (16-bit) or 128 B (fp32) of the 128 B row
             constexpr int QPH = 32 * static_cast<int>(sizeof(OutT)) / 16;  // 16 B chunks per half
 #pragma unroll
