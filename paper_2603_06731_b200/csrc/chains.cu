@@ -213,6 +213,7 @@ cudaError_t softmax_launch_direct(const void* x, void* y, int64_t rows, int64_t 
 // per SM), not in registers, so HBM stays saturated.
 constexpr int STREAM_WARPS = 15;  // + 1 producer warp = 16 warps: 128 registers per thread
 constexpr int STREAM_SMEM = 160 * 1024;
+constexpr int STREAM_SMEM_LN = 192 * 1024;  // layernorm: 2 rows x (x, residual) per slot
 
 __device__ __forceinline__ float ex2f_approx(float x) {
   float y;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     stream_rows_kernel(const TI* __restrict__ x, const TI* __restrict__ res,
                        const float* __restrict__ gamma, const float* __restrict__ beta,
                        TO* __restrict__ y, TO* __restrict__ sum_out, int64_t rows, int cols,
-                       float eps, int ns, int slot_bytes) {
+                       float eps, int ns, int slot_bytes, int grp) {
   using namespace sm100;
   constexpr int E = Vec<TI>::N;
   extern __shared__ uint8_t smem_raw[];
@@ -254,6 +255,9 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
   const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * per;
   const int64_t nr = max(static_cast<int64_t>(0), min(per, rows - r0));
+  // a ring slot holds `grp` consecutive rows (of x, then of the residual):
+  // fewer, larger bulk copies (the per-copy cost bounds 1.5 KB rows)
+  const int64_t nslots = (nr + grp - 1) / grp;
   const uint32_t row_bytes = static_cast<uint32_t>(cols) * sizeof(TI);
   if (threadIdx.x == 0) {
     for (int i = 0; i < ns; ++i) {
@@ -276,16 +280,19 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     // row one lap earlier, whose own wait completed in an earlier batch, so the
     // parity of the empty barrier it waits on is never two phases stale.
     const int batch = ns < 32 ? ns : 32;
-    for (int64_t b0 = 0; b0 < nr; b0 += batch) {
+    for (int64_t b0 = 0; b0 < nslots; b0 += batch) {
       const int64_t i = b0 + lane;
-      if (lane < batch && i < nr) {
+      if (lane < batch && i < nslots) {
         const int slot = static_cast<int>(i % ns);
         const uint32_t ph = static_cast<uint32_t>((i / ns) & 1);
+        const int64_t row = i * grp;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(grp), nr - row)) * row_bytes;
         mbar_wait(&empty[slot], ph ^ 1);
         uint8_t* dst = smem + static_cast<size_t>(slot) * slot_bytes;
-        mbar_arrive_expect_tx(&full[slot], MODE == 1 && res ? 2 * row_bytes : row_bytes);
-        bulk_load(dst, x + (r0 + i) * cols, row_bytes, &full[slot]);
-        if (MODE == 1 && res) bulk_load(dst + row_bytes, res + (r0 + i) * cols, row_bytes, &full[slot]);
+        mbar_arrive_expect_tx(&full[slot], MODE == 1 && res ? 2 * bytes : bytes);
+        bulk_load(dst, x + (r0 + row) * cols, bytes, &full[slot]);
+        if (MODE == 1 && res)
+          bulk_load(dst + grp * row_bytes, res + (r0 + row) * cols, bytes, &full[slot]);
       }
       __syncwarp();
     }
@@ -335,12 +342,10 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
     }
   } else {
-    // residual + layernorm, two rows per warp at a time (rows i and i + 15 of
-    // this warp's stride): the two rows' reduction chains interleave, which
-    // hides the shuffle / smem latency a single row per warp leaves exposed.
-    // Needs ns >= R * STREAM_WARPS (checked at launch) so the rows sit in
-    // different ring slots.
-    constexpr int R = CH <= 4 ? 2 : 1;  // long rows: one at a time (registers)
+    // residual + layernorm, the R rows of a slot per warp: the rows' reduction
+    // chains interleave, which hides the shuffle / smem latency a single row
+    // per warp leaves exposed.
+    constexpr int R = CH <= 4 ? 2 : 1;  // rows per slot (= grp at launch); long rows: 1
     const uint32_t gb_addr = smem_u32(gb);
     // a lane always owns the same columns (chunks lane + 32 k): its gamma / beta
     // live in registers for the whole kernel (rows of <= 768 16-bit columns)
@@ -364,29 +369,28 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
     }
-    for (int64_t i0 = warp; i0 < nr; i0 += STREAM_WARPS * R) {
+    for (int64_t si = warp; si < nslots; si += STREAM_WARPS) {
+      const int slot = static_cast<int>(si % ns);
+      mbar_wait(&full[slot], static_cast<uint32_t>((si / ns) & 1));
+      const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
+      const int64_t i0 = si * R;
       float v[R][CH][E];
       bool have[R];
-      int slot[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int64_t i = i0 + r * STREAM_WARPS;
-        have[r] = i < nr;
-        slot[r] = static_cast<int>(i % ns);
+        have[r] = i0 + r < nr;
         if (!have[r]) continue;
-        mbar_wait(&full[slot[r]], static_cast<uint32_t>((i / ns) & 1));
-        const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot[r]) * slot_bytes);
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
           const int c = lane + 32 * k;
           if (c < nchunks) {
             Vec<TI> t;
-            t.u = ld_shared_v4(sx + c * 16);
+            t.u = ld_shared_v4(sx + r * row_bytes + c * 16);
 #pragma unroll
             for (int e = 0; e < E; ++e) v[r][k][e] = OutCvt<TI>::from(t.e[e]);
             if (res) {
               Vec<TI> q;
-              q.u = ld_shared_v4(sx + row_bytes + c * 16);
+              q.u = ld_shared_v4(sx + (R + r) * row_bytes + c * 16);
 #pragma unroll
               for (int e = 0; e < E; ++e) v[r][k][e] += OutCvt<TI>::from(q.e[e]);
             }
@@ -394,11 +398,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (have[r]) mbar_arrive(&empty[slot[r]]);  // rows consumed: slots refill
-      }
+      if (lane == 0) mbar_arrive(&empty[slot]);  // slot consumed: it refills
       // sums as short trees (one partial per chunk), both rows' shuffles interleaved
       float s[R], q[R], mean[R], rstd[R];
 #pragma unroll
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!have[r]) continue;
-          const int64_t row = r0 + i0 + r * STREAM_WARPS;
+          const int64_t row = r0 + i0 + r;
           Vec<TO> o, so;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
@@ -504,18 +504,21 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
                             reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(so);
   if (addr_or & 15) return cudaErrorNotSupported;
   const int64_t nchunks = cols / E;
-  const int slot_bytes = static_cast<int>(((MODE == 1 && r ? 2 : 1) * cols * sizeof(TI) + 127) / 128 * 128);
+  // layernorm rows of <= 1024 16-bit values: two consecutive rows per ring
+  // slot (one bulk copy each for x and the residual) and per consumer warp
+  const int grp = MODE == 1 && nchunks <= 128 ? 2 : 1;
+  const int64_t row_bytes = cols * static_cast<int64_t>(sizeof(TI));
+  const int slot_bytes =
+      static_cast<int>(((MODE == 1 && r ? 2 : 1) * grp * row_bytes + 127) / 128 * 128);
   // Ring depth is a multiple of the consumer-warp count: consumer warp w takes
-  // rows w, w+15, ..., so the row one lap before row i (i - ns) is its own and
-  // was already consumed (loaded) when it waits on row i. Otherwise a warp can
-  // poll slot i % ns while row i - ns's bulk copy is still in flight (copies
-  // complete out of order) and the parity wait passes one phase early.
-  const int ns = static_cast<int>(std::min<int64_t>(90, STREAM_SMEM / slot_bytes)) /
+  // slots w, w+15, ..., so the slot use one lap before slot i (i - ns) is its
+  // own and was already consumed (loaded) when it waits on slot i. Otherwise a
+  // warp can poll slot i % ns while use i - ns's bulk copy is still in flight
+  // (copies complete out of order) and the parity wait passes a phase early.
+  const int64_t budget = MODE == 1 ? STREAM_SMEM_LN : STREAM_SMEM;
+  const int ns = static_cast<int>(std::min<int64_t>(90, budget / slot_bytes)) /
                  STREAM_WARPS * STREAM_WARPS;
-  // layernorm consumes two rows per warp at a time (rows of <= 1024 16-bit
-  // values): two ring laps of warps
-  const int lanes_rows = MODE == 1 && nchunks <= 128 ? 2 : 1;
-  if (ns < lanes_rows * STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;
+  if (ns < STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;
   const int smem = ns * slot_bytes + ns * 16 + 128 + (MODE == 1 ? static_cast<int>(cols) * 8 + 16 : 0);
   const TI* xi = reinterpret_cast<const TI*>(x);
   const TI* ri = reinterpret_cast<const TI*>(r);
@@ -525,7 +528,7 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, (STREAM_WARPS + 1) * 32, smem, s>>>(xi, ri, g, b, yo, soo, rows, (int)cols, eps, ns,
-                                                     slot_bytes);
+                                                     slot_bytes, grp);
     return cudaGetLastError();
   };
   cudaError_t e;
