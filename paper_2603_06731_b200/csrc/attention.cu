@@ -53,6 +53,7 @@ struct AttnArgs {
   float scale_log2;  // scale * log2(e)
   int causal;
   int o_dtype;
+  int head_group;  // unit order: heads per group (see decode)
   int dbg;  // profiling aid (AFG_ATTN_DEBUG): 1 = no softmax math, 2 = no MMAs,
            // 3 = MMAs back to back (no softmax dependency)
 };
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(384, 1)
     int bh, hh, bb, q0, nkv0, nkv1;
   };
   auto decode = [&](int lin) {
-    constexpr int HEAD_GROUP = 16;
+    const int HEAD_GROUP = args.head_group;
     Unit w;
     const int grp = lin / (HEAD_GROUP * n_pairs);
     const int gsize = min(HEAD_GROUP, args.BH - grp * HEAD_GROUP);
@@ -1080,6 +1081,15 @@ afg_status attention_core(const void* q, const void* k, const void* v, const flo
       return e ? atoi(e) : 0;
     }();
     a.dbg = dbg;
+    // Non-causal units are equal: group heads by 16 so co-resident CTAs share
+    // K/V in L2. Causal: one group = a globally heaviest-first order (the K/V
+    // of all heads ~ fits L2 at the BASELINE shape), which the snake walk
+    // turns into balanced per-CTA totals with the lightest units last.
+    static const int hg_env = [] {
+      const char* e = getenv("AFG_ATTN_HEAD_GROUP");
+      return e ? atoi(e) : 0;
+    }();
+    a.head_group = hg_env > 0 ? hg_env : (causal ? static_cast<int>(BH) : 16);
     cudaError_t e;
     if (pair)
       e = dt == AFG_BF16 ? launch_pair<true>(tq, tk, tv, a, s) : launch_pair<false>(tq, tk, tv, a, s);
