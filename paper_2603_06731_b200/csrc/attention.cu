@@ -562,359 +562,6 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-// ------------------------------------------------ 2-CTA (CTA pair) kernel --
-// A cluster of two CTAs on one TPC issues every MMA as ONE cta_group::2
-// instruction with M = 256: query rows from both CTAs, the K / V tile split
-// between them (each CTA stages half of the keys of K and half of the head
-// dimension of V). Per SM that halves the shared-memory operand traffic of the
-// single-CTA kernel (whose S = Q K^T MMA reads 8 KB of smem per 64-cycle
-// instruction, the whole smem bandwidth) and halves the K / V bytes each SM
-// loads. Softmax / correction / epilogue are per CTA on its own TMEM rows.
-//
-// Pair unit = one (b, h) x 512 query rows: CTA r holds tile A rows
-// [q0 + 128 r, +128) and tile B rows [q0 + 256 + 128 r, +128); MMA group g
-// covers tile g of both CTAs (KV range = the later tile's under causal masking;
-// the earlier tile masks the extra diagonal tile).
-// Warps per CTA: 0 TMA, 1 MMA issuer (leader CTA only), 2 TMEM allocator,
-// 4-7 softmax group A, 8-11 softmax group B.
-struct PairSmem {
-  static constexpr int D = 128;
-  static constexpr int QTILE = BM * D * 2;        // 32 KB
-  static constexpr int HALF = (BN / 2) * D * 2;   // 16 KB: half a K or V tile
-  static constexpr int STAGES = 10;               // K/V half-tile ring
-  static constexpr int QA_OFF = 0;
-  static constexpr int QB_OFF = QTILE;
-  static constexpr int RING_OFF = 2 * QTILE;
-  static constexpr int BAR_OFF = RING_OFF + STAGES * HALF;
-  // q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_done
-  static constexpr int NUM_BARS = 1 + 2 * STAGES + 5;
-  static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
-  static_assert(TOTAL <= 232448, "attention smem over the 227 KB opt-in limit");
-};
-
-template <bool BF16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
-    attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ,
-                     const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const AttnArgs args) {
-  using L = PairSmem;
-  constexpr int D = L::D;
-  constexpr int NS = L::STAGES;
-  constexpr int NCH = BN / 32;
-  constexpr uint32_t TMEM_COLS = 512;
-  constexpr int UNIT = 4 * BM;  // query rows per pair
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + NS;
-  uint64_t* s_full = kv_empty + NS;  // [2]
-  uint64_t* p_full = s_full + 2;     // [2] (leader's counts both CTAs' warps)
-  uint64_t* o_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
-
-  const int warp = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_ctarank();
-
-  const int n_units = (args.Nq + UNIT - 1) / UNIT;
-  constexpr int HEAD_GROUP = 16;  // dispatch order as in attn_fwd_kernel, per pair
-  const int blk = static_cast<int>(blockIdx.x) / 2;
-  const int grp = blk / (HEAD_GROUP * n_units);
-  const int gsize = min(HEAD_GROUP, args.BH - grp * HEAD_GROUP);
-  const int off = blk - grp * HEAD_GROUP * n_units;
-  const int qu = n_units - 1 - off / gsize;
-  const int bh = grp * HEAD_GROUP + off % gsize;
-  const int hh = bh % args.H;
-  const int bb = bh / args.H;
-  const int q0 = qu * UNIT;
-  const int nkv_all = (args.Nk + BN - 1) / BN;
-  auto tiles_of = [&](int first) {
-    return first >= args.Nq ? 0 : args.causal ? min(nkv_all, (first + BM - 1) / BN + 1) : nkv_all;
-  };
-  // group g = tile g of both CTAs: the KV range of the later (rank-1) tile
-  const int nkv0 = max(tiles_of(q0), tiles_of(q0 + BM));
-  const int nkv1 = max(tiles_of(q0 + 2 * BM), tiles_of(q0 + 3 * BM));
-  const int nkv_max = max(nkv0, nkv1);
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-    }
-    for (int g = 0; g < 2; ++g) {
-      mbar_init(&s_full[g], 1);
-      mbar_init(&p_full[g], 8);  // one arrival per softmax warp of both CTAs
-    }
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  auto s_col = [](int g) { return static_cast<uint32_t>(g * BN); };
-  auto o_col = [](int g) { return static_cast<uint32_t>(2 * BN + g * D); };
-
-  if (warp >= 4) {
-    setmaxnreg_inc<224>();
-    // --------------------------------- softmax / correction / epilogue (per tile)
-    const int g = (warp - 4) / 4;
-    const int w4 = warp % 4;
-    const int row = w4 * 32 + lane;
-    const int tile_first = q0 + g * 2 * BM + static_cast<int>(rank) * BM;
-    const int qi = tile_first + row;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
-    const uint32_t s_base = lane_base + s_col(g);
-    const uint32_t o_base = lane_base + o_col(g);
-    const int nkv_g = g ? nkv1 : nkv0;
-    const float* brow =
-        args.bias ? args.bias + (static_cast<int64_t>(bh) * args.Nq + min(qi, args.Nq - 1)) *
-                                    args.Nk
-                  : nullptr;
-    float m = -INFINITY;  // running max (scaled log2 units)
-    float l = 0.0f;
-    auto release_p = [&]() {  // this warp's P (or nothing) is in TMEM
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (rank == 0) mbar_arrive(&p_full[g]);
-        else mbar_arrive_cluster(&p_full[g], 0);
-      }
-    };
-    for (int j = 0; j < (args.dbg == 3 ? 0 : nkv_g); ++j) {
-      mbar_wait(&s_full[g], j & 1);  // also implies PV(g, j-1) completed (in-order MMAs)
-      tc_fence_after();
-      if (args.dbg == 1) {
-        release_p();
-        continue;
-      }
-      uint32_t s[NCH][32];
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) tmem_ld32(s_base + c * 32, s[c]);
-      tmem_wait_ld();
-      const int k0 = j * BN;
-      const bool need_mask = (args.causal && k0 + BN - 1 > tile_first) || k0 + BN > args.Nk;
-      const bool fast = brow == nullptr && !need_mask && args.scale_log2 > 0.0f;
-      float tmax, sc;
-      if (fast) {
-        float mc[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          mc[c] = fmax3(__uint_as_float(s[c][0]), __uint_as_float(s[c][1]),
-                        __uint_as_float(s[c][2]));
-#pragma unroll
-          for (int e = 3; e < 31; e += 2)
-            mc[c] = fmax3(mc[c], __uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1]));
-          mc[c] = fmaxf(mc[c], __uint_as_float(s[c][31]));
-        }
-        tmax = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])) * args.scale_log2;
-        sc = args.scale_log2;
-      } else {
-        tmax = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int kj = k0 + c * 32 + e;
-            float v = __uint_as_float(s[c][e]) * args.scale_log2;
-            if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
-            if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
-            s[c][e] = __float_as_uint(v);
-            tmax = fmaxf(tmax, v);
-          }
-        sc = 1.0f;
-      }
-      const float m_cand = fmaxf(m, tmax);
-      const bool upd = m == -INFINITY || m_cand > m + 8.0f;
-      const float m_new = upd ? m_cand : m;
-      const float base = m_new == -INFINITY ? 0.0f : m_new;
-      const float alpha = upd ? ex2(m - base) : 1.0f;
-      if (j > 0 && __any_sync(0xffffffffu, upd)) {
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(o_base + c * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(o_base + c * 32, o);
-        }
-      }
-      m = m_new;
-      const uint64_t sc2 = f2(sc, sc), nb2 = f2(-base, -base);
-      uint64_t acc2 = f2(0.0f, 0.0f);
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float x0, x1;
-          f2split(ffma2(f2(__uint_as_float(s[c][2 * e]), __uint_as_float(s[c][2 * e + 1])), sc2,
-                        nb2),
-                  x0, x1);
-          const float p0 = ex2(x0), p1 = ex2(x1);
-          acc2 = fadd2(acc2, f2(p0, p1));
-          pk[e] = pack2(p0, p1, BF16);
-        }
-        tmem_st16(s_base + c * 16, pk);
-      }
-      float a0, a1;
-      f2split(acc2, a0, a1);
-      tmem_wait_st();
-      l = l * alpha + (a0 + a1);
-      release_p();
-    }
-    // ---- epilogue: O / l -> global
-    mbar_wait(o_done, 0);
-    tc_fence_after();
-    const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
-    const bool valid = qi < args.Nq && nkv_g > 0;
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(o_base + c * 32, o);
-      tmem_wait_ld();
-      if (!valid) continue;
-      const int64_t base_idx = static_cast<int64_t>(bb) * args.o_bs +
-                               static_cast<int64_t>(hh) * args.o_hs +
-                               static_cast<int64_t>(qi) * args.o_ss + c * 32;
-      if (args.o_dtype == AFG_F32) {
-        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + base_idx);
-#pragma unroll
-        for (int v = 0; v < 8; ++v)
-          dst[v] = make_float4(__uint_as_float(o[4 * v]) * inv_l, __uint_as_float(o[4 * v + 1]) * inv_l,
-                               __uint_as_float(o[4 * v + 2]) * inv_l,
-                               __uint_as_float(o[4 * v + 3]) * inv_l);
-      } else {
-        const bool ob = args.o_dtype == AFG_BF16;
-        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + base_idx);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 u;
-          u.x = pack2(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l, ob);
-          u.y = pack2(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l, ob);
-          u.z = pack2(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l, ob);
-          u.w = pack2(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l, ob);
-          dst[v] = u;
-        }
-      }
-    }
-  } else {
-    setmaxnreg_dec<56>();
-    if (warp == 0) {
-      // ------------------------------------------------------------- TMA --
-      // both CTAs load their halves; completion lands on the LEADER's full
-      // barriers (which expect the bytes of both CTAs)
-      if (lane == 0) {
-        const uint32_t q_bar = mapa_shared(q_full, 0);
-        if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * 2 * L::QTILE);
-        for (int g = 0; g < 2; ++g)
-          for (int a = 0; a < 2; ++a)
-            tma_load_4d_pair(smem + (g ? L::QB_OFF : L::QA_OFF) + a * (BM * 128), &tmQ, q_bar,
-                             a * 64, q0 + g * 2 * BM + static_cast<int>(rank) * BM, hh, bb);
-        for (int n = 0; n < 2 * nkv_max; ++n) {  // item 2j = K(j) half, 2j+1 = V(j) half
-          const int st = n % NS;
-          mbar_wait(&kv_empty[st], ((n / NS) & 1) ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&kv_full[st], 2 * L::HALF);
-          const uint32_t bar = mapa_shared(&kv_full[st], 0);
-          uint8_t* dst = smem + L::RING_OFF + st * L::HALF;
-          const int j = n >> 1;
-          if ((n & 1) == 0) {  // K: keys [64 rank, +64) of tile j, all of D
-            for (int a = 0; a < 2; ++a)
-              tma_load_4d_pair(dst + a * ((BN / 2) * 128), &tmK, bar, a * 64,
-                               j * BN + static_cast<int>(rank) * (BN / 2), hh, bb);
-          } else {  // V: all keys of tile j, head-dim columns [64 rank, +64)
-            tma_load_4d_pair(dst, &tmV, bar, static_cast<int>(rank) * 64, j * BN, hh, bb);
-          }
-        }
-      }
-    } else if (warp == 1) {
-      // ------------------------------------------- MMA (leader CTA only) --
-      if (rank == 0) {  // whole warp, one elected lane issues (see attn_fwd_kernel)
-        const bool leader = elect_one();
-        constexpr uint32_t idesc_s = idesc_f16(2 * BM, BN, BF16 ? 1u : 0u, 0u, 0u);
-        constexpr uint32_t idesc_o = idesc_f16(2 * BM, D, BF16 ? 1u : 0u, 0u, 1u);
-        const uint64_t q_desc0 = desc_kmajor_sw128(smem_u32(smem + L::QA_OFF));
-        const uint64_t k_desc0 = desc_kmajor_sw128(smem_u32(smem + L::RING_OFF));
-        const uint64_t v_desc0 = desc_mnmajor_sw128(smem_u32(smem + L::RING_OFF), BN * 128);
-        constexpr uint64_t QB_STEP = (L::QB_OFF - L::QA_OFF) >> 4;
-        constexpr uint64_t SLOT_STEP = L::HALF >> 4;
-        auto wait_item = [&](int n) {
-          mbar_wait(&kv_full[n % NS], (n / NS) & 1);
-          tc_fence_after();
-        };
-        auto issue_s = [&](int g, int j) {
-          const uint64_t qd = q_desc0 + (g ? QB_STEP : 0);
-          const uint64_t kd = k_desc0 + static_cast<uint64_t>((2 * j) % NS) * SLOT_STEP;
-          if (args.dbg != 2) {
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              mma_f16_ss_if<2>(leader, tmem + s_col(g),
-                               qd + static_cast<uint64_t>(((kk / 4) * (BM * 128) + (kk % 4) * 32) >> 4),
-                               kd + static_cast<uint64_t>(((kk / 4) * ((BN / 2) * 128) + (kk % 4) * 32) >> 4),
-                               idesc_s, kk > 0 ? 1u : 0u);
-          }
-          mma_commit_pair_if(leader, &s_full[g], 3);
-        };
-        auto issue_pv = [&](int g, int j) {
-          const uint64_t vd = v_desc0 + static_cast<uint64_t>((2 * j + 1) % NS) * SLOT_STEP;
-          if (args.dbg == 2) return;
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            mma_f16_ts_if<2>(leader, tmem + o_col(g), tmem + s_col(g) + kk * 8,
-                             vd + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_o,
-                             (j > 0 || kk > 0) ? 1u : 0u);
-        };
-        mbar_wait(q_full, 0);
-        wait_item(0);
-        if (nkv0 > 0) issue_s(0, 0);
-        if (nkv1 > 0) issue_s(1, 0);
-        mma_commit_pair_if(leader, &kv_empty[0], 3);
-        for (int j = 0; j < nkv_max; ++j) {
-          const int jn = j + 1;
-          bool k_next_ready = false;
-          wait_item(2 * j + 1);
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            const int nkv_g = g ? nkv1 : nkv0;
-            if (j < nkv_g) {
-              if (args.dbg != 3) mbar_wait_cluster(&p_full[g], j & 1);
-              tc_fence_after();
-              issue_pv(g, j);
-              if (jn < nkv_g) {
-                if (!k_next_ready) {
-                  wait_item(2 * jn);
-                  k_next_ready = true;
-                }
-                issue_s(g, jn);
-              }
-            }
-          }
-          mma_commit_pair_if(leader, &kv_empty[(2 * j + 1) % NS], 3);
-          if (k_next_ready) mma_commit_pair_if(leader, &kv_empty[(2 * jn) % NS], 3);
-        }
-        mma_commit_pair_if(leader, o_done, 3);
-      }
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync();  // the peer's MMAs / arrivals into this CTA are done
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc_pair<TMEM_COLS>(tmem);
-  }
-}
-
 // ----------------------------------------------------------- SIMT fallback --
 // Any D / dtype / length: one CTA per (bh, query row); scores staged in smem.
 template <typename T>
@@ -989,22 +636,6 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
   return cudaGetLastError();
 }
 
-template <bool BF16>
-cudaError_t launch_pair(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const AttnArgs& a, cudaStream_t s) {
-  auto kern = attn_pair_kernel<BF16>;
-  constexpr int smem = PairSmem::TOTAL;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  const unsigned grid = 2u * static_cast<unsigned>(a.BH) * ((a.Nq + 4 * BM - 1) / (4 * BM));
-  kern<<<grid, 384, smem, s>>>(tq, tk, tv, a);
-  count_launch();
-  return cudaGetLastError();
-}
 
 }  // namespace
 }  // namespace afg
@@ -1043,12 +674,6 @@ afg_status attention_core(const void* q, const void* k, const void* v, const flo
     const CUtensorMapDataType tdt =
         dt == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     CUtensorMap tq, tk, tv;
-    static const bool use_pair = [] {
-      const char* e = getenv("AFG_ATTN_PAIR");
-      return e && atoi(e) != 0;
-    }();
-    // the CTA-pair kernel (D = 128, more than one 256-row query block)
-    const bool pair = D == 128 && Nq > 2 * BM && use_pair;
     uint32_t box[4] = {64, 128, 1, 1};
     auto map4 = [&](CUtensorMap* m, const void* base, int64_t N, Strides str) {
       const uint64_t dims[4] = {static_cast<uint64_t>(D), static_cast<uint64_t>(N),
@@ -1059,9 +684,7 @@ afg_status attention_core(const void* q, const void* k, const void* v, const flo
       return make_tmap(m, base, tdt, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     };
     if ((st = map4(&tq, q, Nq, sq)) != AFG_OK) return st;
-    if (pair) box[1] = BN / 2;  // each CTA of the pair stages half the keys of K
     if ((st = map4(&tk, k, Nk, sk)) != AFG_OK) return st;
-    box[1] = 128;
     if ((st = map4(&tv, v, Nk, sv)) != AFG_OK) return st;
     AttnArgs a;
     a.bias = bias;
@@ -1091,9 +714,7 @@ afg_status attention_core(const void* q, const void* k, const void* v, const flo
     }();
     a.head_group = hg_env > 0 ? hg_env : (causal ? static_cast<int>(BH) : 16);
     cudaError_t e;
-    if (pair)
-      e = dt == AFG_BF16 ? launch_pair<true>(tq, tk, tv, a, s) : launch_pair<false>(tq, tk, tv, a, s);
-    else if (D == 128)
+    if (D == 128)
       e = dt == AFG_BF16 ? launch_tc<128, true>(tq, tk, tv, a, s) : launch_tc<128, false>(tq, tk, tv, a, s);
     else
       e = dt == AFG_BF16 ? launch_tc<64, true>(tq, tk, tv, a, s) : launch_tc<64, false>(tq, tk, tv, a, s);

@@ -71,17 +71,17 @@ def test_full_config_sampled_heads(cuda):
     attn_case(8, 16, 2048, 128, causal=True, heads=np.array([0, 127]))
 
 
-# D = 128 with more than 256 query rows runs the CTA-pair (cta_group::2)
-# kernel: 512 query rows per pair, ragged units, ragged keys, bias, bf16.
+# D = 128 with several 256-row units per head on the persistent kernel: ragged
+# units, ragged keys, bias, bf16 (units cross CTAs' snake walk).
 @pytest.mark.parametrize("N,causal,Nk", [(384, False, None), (384, True, None),
                                          (640, True, None), (1024, False, None),
                                          (1024, True, None), (512, False, 700),
                                          (768, True, 900)])
-def test_pair_kernel_fp16(cuda, N, causal, Nk):
+def test_multi_unit_fp16(cuda, N, causal, Nk):
     attn_case(1, 3, N, 128, causal=causal, Nk=Nk, scale=128 ** -0.5)
 
 
-def test_pair_kernel_bias_bf16(cuda):
+def test_multi_unit_bias_bf16(cuda):
     attn_case(1, 2, 512, 128, bias=True, scale=128 ** -0.5)
     attn_case(2, 2, 768, 128, causal=True, dt=torch.bfloat16, scale=128 ** -0.5)
 
