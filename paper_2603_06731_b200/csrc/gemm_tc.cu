@@ -69,7 +69,9 @@ struct SmemLayout {
   static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;
   static constexpr int EPI_BUFS = EPI_OFFSET + 4 * BLOCK_M * 128 + 2048 <= 232448 ? 2 : 1;
   static constexpr int EPI_BYTES = 2 * EPI_BUFS * BLOCK_M * 128;
-  static constexpr int BAR_OFFSET = EPI_OFFSET + EPI_BYTES;
+  // bias of the tile columns of both epilogue groups (<= max(BLOCK_N, 128))
+  static constexpr int BIAS_OFFSET = EPI_OFFSET + EPI_BYTES;
+  static constexpr int BAR_OFFSET = BIAS_OFFSET + (BLOCK_N > 128 ? BLOCK_N : 128) * 4;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TOTAL = BAR_OFFSET + NUM_BARS * 8 + 16 + 1024;  // +1024 align slack
 };
@@ -146,18 +148,21 @@ __device__ __forceinline__ void store_chunk32(const uint32_t (&acc)[32], const G
 }
 
 // act(acc + bias) (+ residual) for 32 consecutive columns of one row, in fp32.
+// `sbias` (optional): the 32 bias values already staged in shared memory.
 template <int EPI, typename OutT>
 __device__ __forceinline__ void epi_values32(const uint32_t (&acc)[32], const GemmTcArgs& a,
-                                             int row, int col0, float (&v)[32]) {
+                                             int row, int col0, float (&v)[32],
+                                             const float* sbias = nullptr) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]);
   if constexpr (EPI != AFG_EPI_NONE) {
     if (col0 + 32 <= a.N) {
       // bias add and activation on f32x2 pairs (one issue slot per pair)
       const float4* b4 = reinterpret_cast<const float4*>(a.bias + col0);
+      const float4* s4 = reinterpret_cast<const float4*>(sbias);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float4 b = __ldg(b4 + j);
+        const float4 b = sbias ? s4[j] : __ldg(b4 + j);
         uint64_t p0 = fadd2(f2(v[4 * j], v[4 * j + 1]), f2(b.x, b.y));
         uint64_t p1 = fadd2(f2(v[4 * j + 2], v[4 * j + 3]), f2(b.z, b.w));
         p0 = apply_act2<EPI>(p0);
@@ -194,12 +199,17 @@ __device__ __forceinline__ void epi_values32(const uint32_t (&acc)[32], const Ge
 
 template <typename OutT>
 __device__ __forceinline__ void epi_values32_rt(const uint32_t (&acc)[32], const GemmTcArgs& a,
-                                                int row, int col0, float (&v)[32]) {
+                                                int row, int col0, float (&v)[32],
+                                                const float* sbias = nullptr) {
   switch (a.epi) {
-    case AFG_EPI_BIAS: epi_values32<AFG_EPI_BIAS, OutT>(acc, a, row, col0, v); break;
-    case AFG_EPI_BIAS_RELU: epi_values32<AFG_EPI_BIAS_RELU, OutT>(acc, a, row, col0, v); break;
-    case AFG_EPI_BIAS_GELU_TANH: epi_values32<AFG_EPI_BIAS_GELU_TANH, OutT>(acc, a, row, col0, v); break;
-    case AFG_EPI_BIAS_GELU_ERF: epi_values32<AFG_EPI_BIAS_GELU_ERF, OutT>(acc, a, row, col0, v); break;
+    case AFG_EPI_BIAS: epi_values32<AFG_EPI_BIAS, OutT>(acc, a, row, col0, v, sbias); break;
+    case AFG_EPI_BIAS_RELU: epi_values32<AFG_EPI_BIAS_RELU, OutT>(acc, a, row, col0, v, sbias); break;
+    case AFG_EPI_BIAS_GELU_TANH:
+      epi_values32<AFG_EPI_BIAS_GELU_TANH, OutT>(acc, a, row, col0, v, sbias);
+      break;
+    case AFG_EPI_BIAS_GELU_ERF:
+      epi_values32<AFG_EPI_BIAS_GELU_ERF, OutT>(acc, a, row, col0, v, sbias);
+      break;
     default: epi_values32<AFG_EPI_NONE, OutT>(acc, a, row, col0, v); break;
   }
 }
@@ -418,9 +428,21 @@ __global__ void __launch_bounds__(384, 1)
       uint8_t* stage_base = smem + L::EPI_OFFSET + eg * L::EPI_BUFS * (BLOCK_M * 128);
       int staged = 0;  // chunks this group has staged (buffer = staged & 1)
       const bool leader = ew == 0 && lane == 0;
+      // the group's bias columns (chunks eg, eg + 2, ...), staged in smem once
+      // per tile: thread t of the group owns column t of that list; its global
+      // load is issued before the accumulator wait, so its latency hides
+      constexpr int NCHUNK = BLOCK_N / CW;
+      constexpr int GCOLS = (NCHUNK + 1) / 2 * CW;  // bias columns per group (max)
+      float* sb = reinterpret_cast<float*>(smem + L::BIAS_OFFSET) + eg * GCOLS;
+      const int bcol = (eg + 2 * (rloc / CW)) * CW + rloc % CW;  // tile column of my bias value
+      const bool has_bias =
+          args.epi != AFG_EPI_NONE && rloc < (NCHUNK - eg + 1) / 2 * CW && rloc < GCOLS;
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
+        const int gcol = nb * BLOCK_N + bcol;
+        const float bias_v = has_bias && gcol < args.N ? __ldg(args.bias + gcol) : 0.0f;
+        bool bias_staged = false;
         const int acc = iter & 1;
         mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
         tc_fence_after();
@@ -435,6 +457,10 @@ __global__ void __launch_bounds__(384, 1)
           const bool live = n0 < args.N;  // uniform across the group
           uint8_t* stage = stage_base + (staged % L::EPI_BUFS) * (BLOCK_M * 128);
           const uint32_t srow = smem_u32(stage + rloc * 128);
+          if (!bias_staged) {  // readers of the previous tile's bias passed the last barrier
+            if (has_bias) sb[rloc] = bias_v;
+            bias_staged = true;
+          }
           if (live) {
             if (leader) tma_store_wait_read<L::EPI_BUFS - 1>();  // last store from this buffer
             epi_bar_sync(eg);
@@ -449,7 +475,8 @@ __global__ void __launch_bounds__(384, 1)
           for (int h = 0; h < CW / 32; ++h) {
             if (!live) continue;
             float v[32];
-            epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v);
+            epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v,
+                                  sb + ((cc - eg) / 2) * CW + h * 32);
             // 32 values -> 64 B (16-bit) or 128 B (fp32) of the 128 B row
             constexpr int QPH = 32 * static_cast<int>(sizeof(OutT)) / 16;  // 16 B chunks per half
 #pragma unroll
