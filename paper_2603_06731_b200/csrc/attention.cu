@@ -54,6 +54,7 @@ struct AttnArgs {
   int causal;
   int o_dtype;
   int head_group;  // unit order: heads per group (see decode)
+  int o_st32;      // 16-bit O rows 32-byte aligned: 256-bit stores
   int dbg;  // profiling aid (AFG_ATTN_DEBUG): 1 = no softmax math, 2 = no MMAs,
            // 3 = MMAs back to back (no softmax dependency)
 };
@@ -406,16 +407,24 @@ __global__ void __launch_bounds__(384, 1)
                                  __uint_as_float(o[4 * v + 3]) * inv_l);
         } else {
           const bool ob = args.o_dtype == AFG_BF16;
-          uint4* dst =
-              reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) + base_idx + c * 32);
+          uint16_t* dst = reinterpret_cast<uint16_t*>(args.o) + base_idx + c * 32;
+          uint32_t w[16];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 q;
-            q.x = pack2(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l, ob);
-            q.y = pack2(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l, ob);
-            q.z = pack2(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l, ob);
-            q.w = pack2(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l, ob);
-            dst[v] = q;
+          for (int v = 0; v < 16; ++v)
+            w[v] = pack2(__uint_as_float(o[2 * v]) * inv_l, __uint_as_float(o[2 * v + 1]) * inv_l, ob);
+          if (args.o_st32) {
+            // 32-byte stores: each thread writes whole sectors of its row (the
+            // rows of a warp are D * 2 bytes apart, so stores do not coalesce)
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * v),
+                           "r"(w[8 * v]), "r"(w[8 * v + 1]), "r"(w[8 * v + 2]), "r"(w[8 * v + 3]),
+                           "r"(w[8 * v + 4]), "r"(w[8 * v + 5]), "r"(w[8 * v + 6]), "r"(w[8 * v + 7])
+                           : "memory");
+          } else {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) d4[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
           }
         }
       }
@@ -699,6 +708,8 @@ afg_status attention_core(const void* q, const void* k, const void* v, const flo
     a.scale_log2 = scale * 1.4426950408889634f;
     a.causal = causal;
     a.o_dtype = od;
+    a.o_st32 = (reinterpret_cast<uintptr_t>(o) % 32 == 0) && so.s % 16 == 0 && so.h % 16 == 0 &&
+               so.b % 16 == 0;
     static const int dbg = [] {
       const char* e = getenv("AFG_ATTN_DEBUG");
       return e ? atoi(e) : 0;
