@@ -50,6 +50,18 @@ def load_peaks():
                 "source": "fallback"}
 
 
+def floor_fields(wl, peaks, k_ms):
+    """Multi-kernel steps mixing tensor- and HBM-bound ops (ResNet convs, the
+    BERT layer): the sum over ops of max(flops / tensor peak, bytes / HBM peak)
+    and the step's fraction of it, next to the tensor-only `frac`."""
+    ops = getattr(wl, "ops_fb", None)
+    if not ops:
+        return {}
+    floor_s = sum(c * max(f / (peaks["bf16_tflops"] * 1e12), b / (peaks["hbm_gbs"] * 1e9))
+                  for c, f, b in ops)
+    return {"op_floor_ms": floor_s * 1e3, "frac_of_op_floor": floor_s * 1e3 / k_ms}
+
+
 def traffic_for(workload):
     try:
         with open(TRAFFIC_FILE) as f:
@@ -399,6 +411,7 @@ class ResNetConvs(_Base):
         b0, b1 = shard_rows(self.batch, rank, world)
         self.b = b1 - b0
         self.layers = []
+        self.ops_fb = []  # (count, flops, bytes) per layer: the per-layer roofline floor
         self.flops_rank = 0.0
         self.alg_bytes_rank = 0.0
         for i, (H, C, OC, k, s, cnt) in enumerate(RESNET50):
@@ -411,6 +424,8 @@ class ResNetConvs(_Base):
             self.layers.append((x, w, bias, y, k, s, pad, cnt))
             self.flops_rank += cnt * 2.0 * self.b * OH * OH * OC * C * k * k
             self.alg_bytes_rank += cnt * 2.0 * (x.numel() + y.numel() + w.numel())
+            self.ops_fb.append((cnt, 2.0 * self.b * OH * OH * OC * C * k * k,
+                                2.0 * (x.numel() + y.numel() + w.numel())))
         self.flops_total = self.flops_rank * self.batch / self.b
 
     def step(self):
@@ -481,6 +496,13 @@ class BertLayer(_Base):
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
         gemm = 2.0 * T * hd * (3 * hd + hd + 2 * ffn)
         attn = 4.0 * self.b * self.heads * self.seq * self.seq * (hd // self.heads)
+        # (count, flops, bytes) per launch: the per-op roofline floor (bf16 bytes)
+        self.ops_fb = [(1, 2.0 * T * hd * 3 * hd, 2.0 * (T * hd + 3 * hd * hd + 3 * T * hd)),
+                       (1, attn, 2.0 * (3 * T * hd + T * hd)),
+                       (1, 2.0 * T * hd * hd, 2.0 * (T * hd + hd * hd + 2 * T * hd)),
+                       (2, 0.0, 2.0 * 3 * T * hd),
+                       (1, 2.0 * T * hd * ffn, 2.0 * (T * hd + hd * ffn + T * ffn)),
+                       (1, 2.0 * T * ffn * hd, 2.0 * (T * ffn + ffn * hd + 2 * T * hd))]
         self.flops_rank = gemm + attn
         self.flops_total = self.flops_rank * self.batch / self.b
         self.alg_bytes_rank = 2.0 * T * hd * 2
@@ -864,7 +886,8 @@ def run_afg(args, wl, rank, world, local):
                              "achieved": achieved, "peak": peak, "unit": unit,
                              "frac": achieved / peak,
                              "peak_source": f"{peaks['source']} (MEASURED_PEAKS.json burst)",
-                             "kernel_ms": k_ms, "traffic": traffic_for(wl.name)},
+                             "kernel_ms": k_ms, "traffic": traffic_for(wl.name),
+                             **floor_fields(wl, peaks, k_ms)},
                 "e2e": {"value": e2e_value, "unit": wl.unit, "ms_per_step": e_ms,
                         "h2d_bytes_per_step": wl.h2d * world, "d2h_bytes_per_step": wl.d2h * world,
                         "path": "pinned host -> cudaMemcpyAsync -> afg C ABI -> D2H"},
