@@ -913,7 +913,10 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   afg_status st = make_tmap_im2col_4d(&tmA, x, tdt, C, W, H, B, lower, upper,
                                       static_cast<int>(sw), static_cast<int>(sh), BLOCK_K, BLOCK_M);
   if (st != AFG_OK) return st;
-  st = make_tmap_2d(&tmB, w, tdt, 2, K, OC, K, BLOCK_K, block_n);
+  // 256 x 256 CTA-pair tiles as for plain GEMMs (each CTA gathers its own 128
+  // output pixels by im2col and half of the filter rows)
+  const bool pair = use_pair_tiles(block_n, M, OC, K);
+  st = make_tmap_2d(&tmB, w, tdt, 2, K, OC, K, BLOCK_K, pair ? block_n / 2 : block_n);
   if (st != AFG_OK) return st;
   GemmTcArgs args{};
   args.M = static_cast<int>(M);
@@ -923,9 +926,9 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   args.bias = bias;
   args.residual = nullptr;
   args.C = y;
-  args.num_m_blocks = static_cast<int>((M + BLOCK_M - 1) / BLOCK_M);
+  args.num_m_blocks = static_cast<int>((M + (pair ? 2 : 1) * BLOCK_M - 1) / ((pair ? 2 : 1) * BLOCK_M));
   args.num_n_blocks = static_cast<int>((OC + block_n - 1) / block_n);
-  args.group_m = GROUP_M;
+  args.group_m = pair ? GROUP_M / 2 : GROUP_M;
   args.epi = static_cast<int>(epi);
   args.c_blocks = static_cast<int>(C / BLOCK_K);
   args.KW = static_cast<int>(KW);
@@ -944,13 +947,23 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   (dt == AFG_BF16                                                                             \
        ? launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, tmC, args, stream) \
        : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, tmC, args, stream))
-  if (block_n == 256)
+#define AFG_CONV_P(ST)                                                                         \
+  (dt == AFG_BF16                                                                              \
+       ? launch_variant<256, ST, false, true, __nv_bfloat16, true, true>(tmA, tmB, tmC, args,   \
+                                                                         stream)               \
+       : launch_variant<256, ST, false, false, __half, true, true>(tmA, tmB, tmC, args, stream))
+  if (pair && K >= 2048)
+    e = AFG_CONV_P(6);
+  else if (pair)
+    e = AFG_CONV_P(5);
+  else if (block_n == 256)
     e = AFG_CONV_V(256, 3);
   else if (block_n == 128)
     e = AFG_CONV_V(128, 5);
   else
     e = AFG_CONV_V(64, 6);
 #undef AFG_CONV_V
+#undef AFG_CONV_P
   return cuda_status(e, "conv_tc launch");
 }
 

@@ -65,6 +65,13 @@ def test_halo_conv_3x3(cuda, B, H, W, C, OC, dt, epi):
     conv_case(B, H, W, C, OC, 3, 1, 1, dt=dt, epi=epi)
 
 
+# im2col convs with OC >= 256 and K >= 768 on CTA-pair 256 x 256 tiles (both
+# CTAs gather their own 128 output pixels); sampled images at full batch.
+@pytest.mark.parametrize("B,H,C,OC,s", [(128, 14, 256, 256, 1), (64, 28, 256, 512, 2)])
+def test_im2col_pair_tiles(cuda, B, H, C, OC, s):
+    conv_case(B, H, H, C, OC, 3, s, 1, images=np.array([0, B // 2 + 1, B - 1]))
+
+
 def test_implicit_gemm_dilation_and_no_epilogue(cuda):
     conv_case(2, 12, 12, 64, 64, 3, 1, 2, dil=2, epi=Epilogue.NONE)
 
