@@ -560,10 +560,13 @@ struct HaloArgs {
   int tiles_per_img, num_m_tiles, c_chunks;
 };
 
-template <int BLOCK_N>
+// RES_B: the whole filter (9 taps x 64 channels x OC <= BLOCK_N) is loaded into
+// smem once per CTA and stays resident (a single 64-channel chunk and OC block):
+// the per-tile L2 traffic is then the input halo alone.
+template <int BLOCK_N, bool RES_B = false>
 struct HaloSmem {
   static constexpr int A_BYTES = (128 + 2 * 64) * 128;  // (R+2) x P pixels at P = 64
-  static constexpr int B_STAGES = BLOCK_N == 64 ? 8 : (BLOCK_N == 128 ? 6 : 4);
+  static constexpr int B_STAGES = RES_B ? 9 : (BLOCK_N == 64 ? 8 : (BLOCK_N == 128 ? 6 : 4));
   static constexpr int B_BYTES = BLOCK_N * 128;  // BLOCK_N rows x 64 channels (one tap)
   static constexpr int B_OFF = 2 * A_BYTES;
   static constexpr int BAR_OFF = B_OFF + B_STAGES * B_BYTES;
@@ -573,11 +576,11 @@ struct HaloSmem {
   static_assert(TOTAL <= 232448, "halo conv smem over the 227 KB opt-in limit");
 };
 
-template <int BLOCK_N, bool AB_BF16, typename OutT>
+template <int BLOCK_N, bool AB_BF16, typename OutT, bool RES_B>
 __global__ void __launch_bounds__(384, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmX,
                      const __grid_constant__ CUtensorMap tmW, const HaloArgs args) {
-  using L = HaloSmem<BLOCK_N>;
+  using L = HaloSmem<BLOCK_N, RES_B>;
   constexpr int NS = L::B_STAGES;
   constexpr uint32_t TMEM_COLS = 2 * BLOCK_N <= 128 ? 128 : (2 * BLOCK_N <= 256 ? 256 : 512);
   extern __shared__ uint8_t smem_raw[];
@@ -631,6 +634,11 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       int ai = 0, bs = 0;
       uint32_t bph = 0;
+      if constexpr (RES_B) {  // the whole filter, once
+        mbar_arrive_expect_tx(&b_full[0], 9 * L::B_BYTES);
+        for (int tap = 0; tap < 9; ++tap)
+          tma_load_2d(smem + L::B_OFF + tap * L::B_BYTES, &tmW, &b_full[0], tap * args.C, 0);
+      }
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int n, oy0, nb;
         coords(t, n, oy0, nb);
@@ -639,6 +647,7 @@ __global__ void __launch_bounds__(384, 1)
           mbar_wait(&a_empty[slot], ((ai >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&a_full[slot], static_cast<uint32_t>(a_bytes));
           tma_load_4d(smem + slot * L::A_BYTES, &tmX, &a_full[slot], cb * 64, -1, oy0 - 1, n);
+          if constexpr (RES_B) continue;
           for (int tap = 0; tap < 9; ++tap) {
             mbar_wait(&b_empty[bs], bph ^ 1);
             mbar_arrive_expect_tx(&b_full[bs], L::B_BYTES);
@@ -660,6 +669,10 @@ __global__ void __launch_bounds__(384, 1)
     const uint64_t b_desc0 = desc_kmajor_sw128(smem_u32(smem + L::B_OFF));
     int ai = 0, bs = 0, iter = 0;
     uint32_t bph = 0;
+    if constexpr (RES_B) {
+      mbar_wait(&b_full[0], 0);
+      tc_fence_after();
+    }
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
       const int acc = iter & 1;
       mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
@@ -672,8 +685,12 @@ __global__ void __launch_bounds__(384, 1)
         const uint64_t a_slot = a_desc0 + static_cast<uint64_t>(slot) * (L::A_BYTES >> 4);
         for (int tap = 0; tap < 9; ++tap) {
           const int ky = tap / 3, kx = tap - 3 * (tap / 3);
-          mbar_wait(&b_full[bs], bph);
-          tc_fence_after();
+          if constexpr (RES_B) {
+            bs = tap;  // resident filter: tap slot
+          } else {
+            mbar_wait(&b_full[bs], bph);
+            tc_fence_after();
+          }
           // tap window: (ky * P + kx) 128-byte pixel rows into the halo
           const uint64_t ad = a_slot + static_cast<uint64_t>((ky * args.P + kx) * 8);
           const uint64_t bd = b_desc0 + static_cast<uint64_t>(bs) * (L::B_BYTES >> 4);
@@ -681,10 +698,12 @@ __global__ void __launch_bounds__(384, 1)
           for (int k = 0; k < 4; ++k)
             mma_f16_ss_if(leader, d_tmem, ad + static_cast<uint64_t>(k * 2), bd + static_cast<uint64_t>(k * 2),
                           idesc, (cb | tap | k) != 0 ? 1u : 0u);
-          mma_commit_if(leader, &b_empty[bs]);
-          if (++bs == NS) {
-            bs = 0;
-            bph ^= 1;
+          if constexpr (!RES_B) {
+            mma_commit_if(leader, &b_empty[bs]);
+            if (++bs == NS) {
+              bs = 0;
+              bph ^= 1;
+            }
           }
         }
         mma_commit_if(leader, &a_empty[slot]);
@@ -1027,12 +1046,14 @@ afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, i
     return cudaGetLastError();
   };
   cudaError_t e;
-#define AFG_HALO(BN)                                                                         \
-  (dt == AFG_BF16 ? go(conv_halo_kernel<BN, true, __nv_bfloat16>, HaloSmem<BN>::TOTAL)      \
-                  : go(conv_halo_kernel<BN, false, __half>, HaloSmem<BN>::TOTAL))
-  if (block_n == 256) e = AFG_HALO(256);
-  else if (block_n == 128) e = AFG_HALO(128);
-  else e = AFG_HALO(64);
+#define AFG_HALO(BN, RB)                                                                         \
+  (dt == AFG_BF16 ? go(conv_halo_kernel<BN, true, __nv_bfloat16, RB>, HaloSmem<BN, RB>::TOTAL)  \
+                  : go(conv_halo_kernel<BN, false, __half, RB>, HaloSmem<BN, RB>::TOTAL))
+  // one channel chunk and one OC block: keep the filter resident
+  const bool res_b = C == 64 && OC <= block_n && block_n <= 128;
+  if (block_n == 256) e = AFG_HALO(256, false);
+  else if (block_n == 128) e = res_b ? AFG_HALO(128, true) : AFG_HALO(128, false);
+  else e = res_b ? AFG_HALO(64, true) : AFG_HALO(64, false);
 #undef AFG_HALO
   return cuda_status(e, "conv_halo launch");
 }
