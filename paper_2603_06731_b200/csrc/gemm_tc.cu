@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(384, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       // PAIR: one arrival per epilogue warp of both CTAs (on the leader's)
-      mbar_init(&tempty_bar[s], PAIR ? 16 : 256);
+      // a tile that is one TMA-store chunk wide (BLOCK_N = 64, 16-bit C) is
+      // handled by one epilogue group, the groups alternating tiles
+      const bool alt = args.tma_store && BLOCK_N * static_cast<int>(sizeof(OutT)) == 128;
+      mbar_init(&tempty_bar[s], PAIR ? 16 : (alt ? 128 : 256));
     }
     fence_barrier_init();
   }
@@ -432,12 +435,17 @@ __global__ void __launch_bounds__(384, 1)
       // per tile: thread t of the group owns column t of that list; its global
       // load is issued before the accumulator wait, so its latency hides
       constexpr int NCHUNK = BLOCK_N / CW;
+      // one chunk per tile: the two groups take alternate tiles (geff = 0 for
+      // both); otherwise they take alternate chunks of every tile
+      constexpr bool ALT = NCHUNK == 1;
+      const int geff = ALT ? 0 : eg;
       constexpr int GCOLS = (NCHUNK + 1) / 2 * CW;  // bias columns per group (max)
       float* sb = reinterpret_cast<float*>(smem + L::BIAS_OFFSET) + eg * GCOLS;
-      const int bcol = (eg + 2 * (rloc / CW)) * CW + rloc % CW;  // tile column of my bias value
+      const int bcol = (geff + 2 * (rloc / CW)) * CW + rloc % CW;  // tile column of my bias value
       const bool has_bias =
-          args.epi != AFG_EPI_NONE && rloc < (NCHUNK - eg + 1) / 2 * CW && rloc < GCOLS;
+          args.epi != AFG_EPI_NONE && rloc < (NCHUNK - geff + 1) / 2 * CW && rloc < GCOLS;
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
+        if (ALT && (iter & 1) != eg) continue;  // the other group's tile
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
         const int gcol = nb * BLOCK_N + bcol;
@@ -450,9 +458,9 @@ __global__ void __launch_bounds__(384, 1)
         const int row = m0 + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
         constexpr int NCH = BLOCK_N / CW;
-        if (eg >= NCH) release_acc(acc);  // no chunk for this group: still release once
+        if (geff >= NCH) release_acc(acc);  // no chunk for this group: still release once
 #pragma unroll 1
-        for (int cc = eg; cc < NCH; cc += 2) {
+        for (int cc = geff; cc < NCH; cc += 2) {
           const int n0 = nb * BLOCK_N + cc * CW;
           const bool live = n0 < args.N;  // uniform across the group
           uint8_t* stage = stage_base + (staged % L::EPI_BUFS) * (BLOCK_M * 128);
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(384, 1)
             if (!live) continue;
             float v[32];
             epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v,
-                                  sb + ((cc - eg) / 2) * CW + h * 32);
+                                  sb + ((cc - geff) / 2) * CW + h * 32);
             // 32 values -> 64 B (16-bit) or 128 B (fp32) of the 128 B row
             constexpr int QPH = 32 * static_cast<int>(sizeof(OutT)) / 16;  // 16 B chunks per half
 #pragma unroll
