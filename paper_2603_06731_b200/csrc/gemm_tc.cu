@@ -67,7 +67,9 @@ struct SmemLayout {
   // C staging: 2 epilogue groups x EPI_BUFS x (128 rows x 128 B); two buffers
   // per group when they fit next to the operand stages
   static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;
-  static constexpr int EPI_BUFS = EPI_OFFSET + 4 * BLOCK_M * 128 + 2048 <= 232448 ? 2 : 1;
+  static constexpr int EPI_BUFS = EPI_OFFSET + 8 * BLOCK_M * 128 + 2048 <= 232448   ? 4
+                                  : EPI_OFFSET + 4 * BLOCK_M * 128 + 2048 <= 232448 ? 2
+                                                                                     : 1;
   static constexpr int EPI_BYTES = 2 * EPI_BUFS * BLOCK_M * 128;
   // bias of the tile columns of both epilogue groups (<= max(BLOCK_N, 128))
   static constexpr int BIAS_OFFSET = EPI_OFFSET + EPI_BYTES;
@@ -901,8 +903,12 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (pair)  // shorter K: the epilogue matters more (5 stages, two C buffers per group)
     e = dispatch_types<256, 5, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+  else if (block_n == 256 && K <= 128)  // output-bound: 2 stages, 4 C buffers per group
+    e = dispatch_types<256, 2>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 256)
     e = dispatch_types<256, 3>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+  else if (block_n == 128 && K <= 128)
+    e = dispatch_types<128, 2>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 128)
     e = dispatch_types<128, 5>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else
