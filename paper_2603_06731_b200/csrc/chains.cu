@@ -266,13 +266,16 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     }
     fence_barrier_init();
   }
+  __syncthreads();  // barriers initialised: the producer starts streaming at once
   if constexpr (MODE == 1) {
-    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-      gb[c] = gamma[c];
-      gb[cols + c] = beta[c];
+    if (warp < STREAM_WARPS) {  // gamma / beta staged by the consumers meanwhile
+      for (int c = threadIdx.x; c < cols; c += STREAM_WARPS * 32) {
+        gb[c] = gamma[c];
+        gb[cols + c] = beta[c];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(STREAM_WARPS * 32) : "memory");
     }
   }
-  __syncthreads();
   if (warp == STREAM_WARPS) {
     // The lanes issue a batch of up to 32 rows in parallel (the mbarrier /
     // bulk-copy issue latency of one row does not serialise the ring), batches
@@ -280,11 +283,13 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     // row one lap earlier, whose own wait completed in an earlier batch, so the
     // parity of the empty barrier it waits on is never two phases stale.
     const int batch = ns < 32 ? ns : 32;
+    // ring position of this lane's slot, advanced by `batch` per round (no
+    // 64-bit divisions in the loop; batch <= ns wraps at most once)
+    int slot = lane % ns;
+    uint32_t ph = 0;
     for (int64_t b0 = 0; b0 < nslots; b0 += batch) {
       const int64_t i = b0 + lane;
       if (lane < batch && i < nslots) {
-        const int slot = static_cast<int>(i % ns);
-        const uint32_t ph = static_cast<uint32_t>((i / ns) & 1);
         const int64_t row = i * grp;
         const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(grp), nr - row)) * row_bytes;
         mbar_wait(&empty[slot], ph ^ 1);
@@ -294,15 +299,32 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         if (MODE == 1 && res)
           bulk_load(dst + grp * row_bytes, res + (r0 + row) * cols, bytes, &full[slot]);
       }
+      slot += batch;
+      if (slot >= ns) {
+        slot -= ns;
+        ph ^= 1;
+      }
       __syncwarp();
     }
     return;
   }
   const int nchunks = cols / E;
+  // consumer ring position (slot, phase) advanced by STREAM_WARPS per row /
+  // slot: ns is a multiple of STREAM_WARPS, so it wraps exactly
+  int cslot = warp;
+  uint32_t cph = 0;
+  auto advance = [&]() {
+    cslot += STREAM_WARPS;
+    if (cslot >= ns) {
+      cslot -= ns;
+      cph ^= 1;
+    }
+  };
+  const float inv_cols = 1.0f / static_cast<float>(cols);
   if constexpr (MODE == 0) {
-    for (int64_t i = warp; i < nr; i += STREAM_WARPS) {
-      const int slot = static_cast<int>(i % ns);
-      mbar_wait(&full[slot], static_cast<uint32_t>((i / ns) & 1));
+    for (int64_t i = warp; i < nr; i += STREAM_WARPS, advance()) {
+      const int slot = cslot;
+      mbar_wait(&full[slot], cph);
       const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
       const int64_t row = r0 + i;
       TO* yr = y + row * cols;
@@ -369,9 +391,9 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
     }
-    for (int64_t si = warp; si < nslots; si += STREAM_WARPS) {
-      const int slot = static_cast<int>(si % ns);
-      mbar_wait(&full[slot], static_cast<uint32_t>((si / ns) & 1));
+    for (int64_t si = warp; si < nslots; si += STREAM_WARPS, advance()) {
+      const int slot = cslot;
+      mbar_wait(&full[slot], cph);
       const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
       const int64_t i0 = si * R;
       float v[R][CH][E];
@@ -427,7 +449,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         for (int r = 0; r < R; ++r) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        mean[r] = s[r] / cols;
+        mean[r] = s[r] * inv_cols;
         float part[CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -452,7 +474,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
 #pragma unroll
         for (int r = 0; r < R; ++r) q[r] += __shfl_xor_sync(0xffffffffu, q[r], o);
 #pragma unroll
-      for (int r = 0; r < R; ++r) rstd[r] = rsqrtf(q[r] / cols + eps);
+      for (int r = 0; r < R; ++r) rstd[r] = rsqrtf(fmaf(q[r], inv_cols, eps));
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int c = lane + 32 * k;
