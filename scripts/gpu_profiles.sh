@@ -35,6 +35,8 @@ cap attention attn_fwd attention
 cap attention_causal attn_fwd attention_causal
 cap softmax stream_rows softmax
 cap layernorm stream_rows layernorm
-cap resnet50_convs gemm_tc resnet_conv
+cap resnet50_convs conv_halo resnet_conv_halo
+cap resnet50_convs gemm_tc resnet_conv_gemm
+cap bert_layer attn_fwd bert_attention
 cap gemm_fp32 gemm_simt gemm_fp32
 echo done > $O/done
