@@ -514,7 +514,9 @@ __global__ void __launch_bounds__(384, 1)
           ++staged;
         }
       }
-      if (leader) tma_store_wait<0>();
+      // the staging smem must outlive the stores' reads; the global writes
+      // themselves complete with the grid (no wait for them at the tail)
+      if (leader) tma_store_wait_read<0>();
     } else {
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         int mb, nb;
