@@ -51,6 +51,10 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
                    afg_dtype ab, afg_dtype c, afg_layout b_layout, afg_epilogue epi,
                    cudaStream_t stream);
 
+// Programmatic dependent launch for the persistent kernels (they wait on the
+// previous grid with griddepcontrol.wait after their prologue); AFG_PDL=0
+// disables it for A/B measurements.
+bool pdl_enabled();
 afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, int64_t B,
                      int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_epilogue epi,
                      cudaStream_t stream);

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -88,6 +89,14 @@ int num_sms() {
 }
 
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("AFG_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
 
 afg_status make_tmap(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int rank,
                      const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,

@@ -229,6 +229,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // Q / K / V from the previous kernel are visible
+  griddep_launch_dependents();
   auto s_col = [](int g) { return static_cast<uint32_t>(g * BN); };
   auto o_col = [](int g) { return static_cast<uint32_t>(2 * BN + g * D); };
 
@@ -640,9 +642,19 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
   }
   const int units = a.BH * ((a.Nq + 2 * BM - 1) / (2 * BM));
   const unsigned grid = static_cast<unsigned>(std::min(units, num_sms()));  // persistent
-  kern<<<grid, 384, smem, s>>>(tq, tk, tv, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see gemm_tc.cu
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, a);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 

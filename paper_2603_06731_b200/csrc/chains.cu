@@ -267,6 +267,8 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     fence_barrier_init();
   }
   __syncthreads();  // barriers initialised: the producer starts streaming at once
+  griddep_wait();   // the previous kernel's output (our input) is visible
+  griddep_launch_dependents();
   if constexpr (MODE == 1) {
     if (warp < STREAM_WARPS) {  // gamma / beta staged by the consumers meanwhile
       for (int c = threadIdx.x; c < cols; c += STREAM_WARPS * 32) {
@@ -549,9 +551,19 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   const unsigned grid = static_cast<unsigned>(num_sms());
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<grid, (STREAM_WARPS + 1) * 32, smem, s>>>(xi, ri, g, b, yo, soo, rows, (int)cols, eps, ns,
-                                                     slot_bytes, grp);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((STREAM_WARPS + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see gemm_tc.cu
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, xi, ri, g, b, yo, soo, rows, (int)cols, eps, ns,
+                                       slot_bytes, grp);
+    return e != cudaSuccess ? e : cudaGetLastError();
   };
   cudaError_t e;
   if (nchunks <= 32) e = go(stream_rows_kernel<TI, TO, MODE, 1>);

@@ -295,6 +295,8 @@ __global__ void __launch_bounds__(384, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // the previous kernel's outputs (our A / B / residual) are visible
+  griddep_launch_dependents();
 
   const int num_tiles = args.num_m_blocks * args.num_n_blocks;
   const int num_kb = (args.K + BLOCK_K - 1) / BLOCK_K;
@@ -632,6 +634,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  griddep_launch_dependents();
   // tile t: output-pixel block mt (image n, rows oy0..oy0+R-1), OC block nb
   // (nb fastest: consecutive tiles reuse the same halo in L2)
   auto coords = [&](int t, int& n, int& oy0, int& nb) {
@@ -764,6 +768,7 @@ __global__ void __launch_bounds__(384, 1)
 
 // --------------------------------------------------------------- host side --
 
+
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT,
           bool IM2COL = false, bool PAIR = false>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
@@ -778,30 +783,33 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
     configured = true;
   }
   const int tiles = args.num_m_blocks * args.num_n_blocks;
-  if constexpr (PAIR) {
-    // persistent CTA pairs (clusters of 2 on one TPC), one per 2 SMs
-    const int clusters = std::min(tiles, num_sms() / 2);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(384);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, args);
-    count_launch();
-    return e != cudaSuccess ? e : cudaGetLastError();
-  } else {
-    const int grid = std::min(tiles, num_sms());
-    kern<<<grid, 384, smem, stream>>>(tmA, tmB, tmC, args);
-    count_launch();
-    return cudaGetLastError();
+  // persistent grid (CTA pairs: clusters of 2 on one TPC, one per 2 SMs),
+  // launched as a programmatic dependent of the previous kernel in the stream
+  const int grid = PAIR ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (PAIR) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, args);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int BLOCK_N, int STAGES, bool PAIR = false>
@@ -1057,9 +1065,19 @@ afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, i
     (void)configured;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, smem, stream>>>(tmX, tmW, a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e2 = cudaLaunchKernelEx(&cfg, kern, tmX, tmW, a);
     count_launch();
-    return cudaGetLastError();
+    return e2 != cudaSuccess ? e2 : cudaGetLastError();
   };
   cudaError_t e;
 #define AFG_HALO(BN, RB)                                                                         \

@@ -580,6 +580,14 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
+// Programmatic dependent launch: wait for the preceding grid's memory (the
+// prologue before it - barrier init, TMEM allocation, descriptor prefetch -
+// overlaps that grid's tail) and let the next grid start its own prologue.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ misc ----
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
