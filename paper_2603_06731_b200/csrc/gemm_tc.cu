@@ -58,22 +58,22 @@ struct GemmTcArgs {
 // PAIR: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile with one
 // cta_group::2 MMA per K step; each CTA stages its 128 rows of A and half of
 // the BLOCK_N rows/columns of B (halving per-SM B traffic in smem and L2).
-template <int BLOCK_N, int STAGES, bool PAIR = false>
+template <int BLOCK_N, int STAGES, bool PAIR = false, int NG = 2>
 struct SmemLayout {
   static constexpr int B_ROWS = PAIR ? BLOCK_N / 2 : BLOCK_N;  // B rows staged per CTA
   static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 2;
   static constexpr int B_BYTES = B_ROWS * BLOCK_K * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // C staging: 2 epilogue groups x EPI_BUFS x (128 rows x 128 B); two buffers
-  // per group when they fit next to the operand stages
+  // C staging: NG epilogue groups x EPI_BUFS x (128 rows x 128 B); more
+  // buffers per group when they fit next to the operand stages
   static constexpr int EPI_OFFSET = STAGES * STAGE_BYTES;
-  static constexpr int EPI_BUFS = EPI_OFFSET + 8 * BLOCK_M * 128 + 2048 <= 232448   ? 4
-                                  : EPI_OFFSET + 4 * BLOCK_M * 128 + 2048 <= 232448 ? 2
-                                                                                     : 1;
-  static constexpr int EPI_BYTES = 2 * EPI_BUFS * BLOCK_M * 128;
-  // bias of the tile columns of both epilogue groups (<= max(BLOCK_N, 128))
+  static constexpr int EPI_BUFS = EPI_OFFSET + 4 * NG * BLOCK_M * 128 + 2048 <= 232448   ? 4
+                                  : EPI_OFFSET + 2 * NG * BLOCK_M * 128 + 2048 <= 232448 ? 2
+                                                                                          : 1;
+  static constexpr int EPI_BYTES = NG * EPI_BUFS * BLOCK_M * 128;
+  // bias of the tile columns of all epilogue groups (<= max(BLOCK_N, NG * 64))
   static constexpr int BIAS_OFFSET = EPI_OFFSET + EPI_BYTES;
-  static constexpr int BAR_OFFSET = BIAS_OFFSET + (BLOCK_N > 128 ? BLOCK_N : 128) * 4;
+  static constexpr int BAR_OFFSET = BIAS_OFFSET + (BLOCK_N > NG * 64 ? BLOCK_N : NG * 64) * 4;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TOTAL = BAR_OFFSET + NUM_BARS * 8 + 16 + 1024;  // +1024 align slack
 };
@@ -238,12 +238,12 @@ __device__ __forceinline__ void store_chunk32_rt(const uint32_t (&acc)[32], cons
 }
 
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT, bool IM2COL,
-          bool PAIR>
-__global__ void __launch_bounds__(384, 1)
+          bool PAIR, int NG>
+__global__ void __launch_bounds__(128 + 128 * NG, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const GemmTcArgs args) {
-  using L = SmemLayout<BLOCK_N, STAGES, PAIR>;
+  using L = SmemLayout<BLOCK_N, STAGES, PAIR, NG>;
   constexpr int TILE_M = PAIR ? 2 * BLOCK_M : BLOCK_M;  // rows per (pair) tile
   static_assert(BLOCK_N % 64 == 0 && BLOCK_N <= 256, "BLOCK_N");
   constexpr uint32_t TMEM_COLS = 2 * BLOCK_N <= 32    ? 32
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(384, 1)
       // a tile that is one TMA-store chunk wide (BLOCK_N = 64, 16-bit C) is
       // handled by one epilogue group, the groups alternating tiles
       const bool alt = args.tma_store && BLOCK_N * static_cast<int>(sizeof(OutT)) == 128;
-      mbar_init(&tempty_bar[s], PAIR ? 16 : (alt ? 128 : 256));
+      mbar_init(&tempty_bar[s], PAIR ? 8 * NG : (alt ? 128 : 128 * NG));
     }
     fence_barrier_init();
   }
@@ -407,8 +407,9 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue --
-    // Two groups of 4 warps (warps 4-7 and 8-11); both cover TMEM lanes 0-127
-    // (warp % 4 selects the 32-lane slice) and take alternate column chunks.
+    // NG groups of 4 warps (warps 4-7, 8-11, ...); each covers TMEM lanes
+    // 0-127 (warp % 4 selects the 32-lane slice); they take column chunks
+    // round-robin.
     const int eg = (warp - 4) / 4;
     const int ew = warp % 4;
     const int rloc = ew * 32 + lane;
@@ -435,21 +436,21 @@ __global__ void __launch_bounds__(384, 1)
       uint8_t* stage_base = smem + L::EPI_OFFSET + eg * L::EPI_BUFS * (BLOCK_M * 128);
       int staged = 0;  // chunks this group has staged (buffer = staged & 1)
       const bool leader = ew == 0 && lane == 0;
-      // the group's bias columns (chunks eg, eg + 2, ...), staged in smem once
+      // the group's bias columns (chunks eg, eg + NG, ...), staged in smem once
       // per tile: thread t of the group owns column t of that list; its global
       // load is issued before the accumulator wait, so its latency hides
       constexpr int NCHUNK = BLOCK_N / CW;
-      // one chunk per tile: the two groups take alternate tiles (geff = 0 for
-      // both); otherwise they take alternate chunks of every tile
+      // one chunk per tile: the groups take tiles round-robin (geff = 0 for
+      // all); otherwise they take chunks of every tile round-robin
       constexpr bool ALT = NCHUNK == 1;
       const int geff = ALT ? 0 : eg;
-      constexpr int GCOLS = (NCHUNK + 1) / 2 * CW;  // bias columns per group (max)
+      constexpr int GCOLS = (NCHUNK + NG - 1) / NG * CW;  // bias columns per group (max)
       float* sb = reinterpret_cast<float*>(smem + L::BIAS_OFFSET) + eg * GCOLS;
-      const int bcol = (geff + 2 * (rloc / CW)) * CW + rloc % CW;  // tile column of my bias value
+      const int bcol = (geff + NG * (rloc / CW)) * CW + rloc % CW;  // tile column of my bias value
       const bool has_bias =
-          args.epi != AFG_EPI_NONE && rloc < (NCHUNK - geff + 1) / 2 * CW && rloc < GCOLS;
+          args.epi != AFG_EPI_NONE && rloc < (NCHUNK - geff + NG - 1) / NG * CW && rloc < GCOLS;
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
-        if (ALT && (iter & 1) != eg) continue;  // the other group's tile
+        if (ALT && iter % NG != eg) continue;  // another group's tile
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
         const int gcol = nb * BLOCK_N + bcol;
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(384, 1)
         constexpr int NCH = BLOCK_N / CW;
         if (geff >= NCH) release_acc(acc);  // no chunk for this group: still release once
 #pragma unroll 1
-        for (int cc = geff; cc < NCH; cc += 2) {
+        for (int cc = geff; cc < NCH; cc += NG) {
           const int n0 = nb * BLOCK_N + cc * CW;
           const bool live = n0 < args.N;  // uniform across the group
           uint8_t* stage = stage_base + (staged % L::EPI_BUFS) * (BLOCK_M * 128);
@@ -482,13 +483,13 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int h = 0; h < CW / 32; ++h) tmem_ld32(t_row + cc * CW + h * 32, rr[h]);
           tmem_wait_ld();
-          if (cc + 2 >= NCH) release_acc(acc);  // last TMEM read of the tile
+          if (cc + NG >= NCH) release_acc(acc);  // last TMEM read of the tile
 #pragma unroll
           for (int h = 0; h < CW / 32; ++h) {
             if (!live) continue;
             float v[32];
             epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v,
-                                  sb + ((cc - geff) / 2) * CW + h * 32);
+                                  sb + ((cc - geff) / NG) * CW + h * 32);
             // 32 values -> 64 B (16-bit) or 128 B (fp32) of the 128 B row
             constexpr int QPH = 32 * static_cast<int>(sizeof(OutT)) / 16;  // 16 B chunks per half
 #pragma unroll
@@ -530,11 +531,11 @@ __global__ void __launch_bounds__(384, 1)
         const int row = mb * TILE_M + static_cast<int>(rank) * BLOCK_M + rloc;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BLOCK_N;
 #pragma unroll 1
-        for (int c = eg; c < BLOCK_N / 32; c += 2) {
+        for (int c = eg; c < BLOCK_N / 32; c += NG) {
           uint32_t r[32];
           tmem_ld32(t_row + c * 32, r);
           tmem_wait_ld();
-          if (c + 2 >= BLOCK_N / 32) release_acc(acc);
+          if (c + NG >= BLOCK_N / 32) release_acc(acc);
           const int col0 = nb * BLOCK_N + c * 32;
           if (col0 < args.N) store_chunk32_rt<OutT>(r, args, row, col0);
         }
@@ -770,11 +771,11 @@ __global__ void __launch_bounds__(384, 1)
 
 
 template <int BLOCK_N, int STAGES, bool B_MN_MAJOR, bool AB_BF16, typename OutT,
-          bool IM2COL = false, bool PAIR = false>
+          bool IM2COL = false, bool PAIR = false, int NG = 2>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmC, const GemmTcArgs& args, cudaStream_t stream) {
-  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL, PAIR>;
-  constexpr int smem = SmemLayout<BLOCK_N, STAGES, PAIR>::TOTAL;
+  auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL, PAIR, NG>;
+  constexpr int smem = SmemLayout<BLOCK_N, STAGES, PAIR, NG>::TOTAL;
   static_assert(smem <= 232448, "gemm smem over the 227 KB opt-in limit");
   static bool configured = false;  // per-instantiation, per-process
   if (!configured) {
@@ -788,7 +789,7 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
   const int grid = PAIR ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(384);
+  cfg.blockDim = dim3(128 + 128 * NG);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -812,12 +813,12 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <int BLOCK_N, int STAGES, bool PAIR = false>
+template <int BLOCK_N, int STAGES, bool PAIR = false, int NG = 2>
 cudaError_t dispatch_types(afg_dtype ab, afg_dtype c, bool b_mn_major, const CUtensorMap& tmA,
                            const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmTcArgs& args,
                            cudaStream_t s) {
 #define AFG_GEMM_V(MN, BF, OT) \
-  launch_variant<BLOCK_N, STAGES, MN, BF, OT, false, PAIR>(tmA, tmB, tmC, args, s)
+  launch_variant<BLOCK_N, STAGES, MN, BF, OT, false, PAIR, NG>(tmA, tmB, tmC, args, s)
   if (ab == AFG_BF16) {
     if (c == AFG_BF16) return b_mn_major ? AFG_GEMM_V(true, true, __nv_bfloat16)
                                          : AFG_GEMM_V(false, true, __nv_bfloat16);
@@ -859,6 +860,20 @@ bool use_pair_tiles(int block_n, int64_t M, int64_t N, int64_t K) {
   if (!enabled || block_n != 256 || M < 256 || K < 768) return false;
   const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
   return pair_tiles >= num_sms() / 2;
+}
+
+// Four epilogue warp groups (640-thread CTA, one C staging buffer per group)
+// for the short-K pair GEMM when the epilogue is GELU: its per-element math,
+// not the store stream, then bounds the tile (BERT FFN1 erf-GELU 145 -> 135 us);
+// bias-only epilogues keep two groups with two buffers each (102 vs 106 us).
+// AFG_GEMM_EPI_GROUPS = 2 | 4 forces either.
+bool four_epi_groups(afg_epilogue epi) {
+  static const int forced = [] {
+    const char* e = getenv("AFG_GEMM_EPI_GROUPS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 2 || forced == 4) return forced == 4;
+  return epi == AFG_EPI_BIAS_GELU_TANH || epi == AFG_EPI_BIAS_GELU_ERF;
 }
 
 }  // namespace
@@ -911,6 +926,8 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   cudaError_t e;
   if (pair && K >= 2048)  // long K: operand stages first (6 x 32 KB, one C buffer per group)
     e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+  else if (pair && four_epi_groups(epi))  // GELU: four epilogue groups, one C buffer each
+    e = dispatch_types<256, 5, true, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (pair)  // shorter K: the epilogue matters more (5 stages, two C buffers per group)
     e = dispatch_types<256, 5, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 256 && K <= 128)  // output-bound: 2 stages, 4 C buffers per group

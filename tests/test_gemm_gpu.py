@@ -160,24 +160,37 @@ def test_many_tiles_per_cta(cuda, N, out):
     run_case(cuda, M, N, 128, out=out, epi=Epilogue.BIAS_RELU, rows=np.arange(0, M, 997))
 
 
-# 256 x 256 tiles on a CTA pair (cta_group::2): BLOCK_N = 256 problems with at
-# least a wave of pair tiles. Ragged M / N, both B layouts, every output type,
-# residual, and >= 3 pair tiles per cluster (accumulator hand-off across both
-# CTAs' epilogues).
+# 256 x 256 tiles on a CTA pair (cta_group::2): BLOCK_N = 256 problems with
+# K >= 768 and at least a wave of pair tiles. Ragged M / N / K, both B layouts,
+# every output type, residual, >= 3 pair tiles per cluster (accumulator hand-off
+# across both CTAs' epilogues), the 5-stage (K < 2048) and 6-stage variants,
+# and both epilogue widths (GELU: four warp groups; bias / ReLU: two).
 PAIR_ROWS = np.array([0, 127, 128, 255, 256, 2047, 3999])
 
 
 @pytest.mark.parametrize("layout", [Layout.B_KN, Layout.B_NK])
 @pytest.mark.parametrize("out", [torch.bfloat16, torch.float32])
 def test_pair_tiles_ragged(cuda, layout, out):
-    run_case(cuda, 4000, 2300, 704, out=out, layout=layout, rows=PAIR_ROWS)
+    run_case(cuda, 4000, 2300, 800, out=out, layout=layout, rows=PAIR_ROWS)
 
 
 def test_pair_tiles_fp16_residual(cuda):
-    run_case(cuda, 4000, 4352, 512, dt=torch.float16, epi=Epilogue.BIAS, residual=True,
+    run_case(cuda, 4000, 4352, 1024, dt=torch.float16, epi=Epilogue.BIAS, residual=True,
              rows=PAIR_ROWS)
 
 
-def test_pair_tiles_many_per_cluster(cuda):
+@pytest.mark.parametrize("epi", [Epilogue.BIAS_RELU, Epilogue.BIAS_GELU_ERF])
+def test_pair_tiles_many_per_cluster(cuda, epi):
     M = 256 * 74 * 3 + 77
-    run_case(cuda, M, 512, 128, epi=Epilogue.BIAS_RELU, rows=np.arange(0, M, 1013))
+    run_case(cuda, M, 512, 768, epi=epi, layout=Layout.B_NK, rows=np.arange(0, M, 1013))
+
+
+@pytest.mark.parametrize("epi", [Epilogue.BIAS, Epilogue.BIAS_GELU_TANH])
+def test_pair_tiles_long_k(cuda, epi):
+    run_case(cuda, 4000, 2300, 2112, epi=epi, rows=PAIR_ROWS)
+
+
+def test_pair_tiles_bert_ffn1_sampled(cuda):
+    """BERT FFN1 at full size (B64 x S512 tokens, 768 -> 3072, erf GELU)."""
+    rows = np.array([0, 1, 255, 256, 16383, 32767])
+    run_case(cuda, 32768, 3072, 768, epi=Epilogue.BIAS_GELU_ERF, layout=Layout.B_NK, rows=rows)
