@@ -848,18 +848,20 @@ int make_store_map(CUtensorMap* map, void* C, afg_dtype c, int64_t M, int64_t N,
 }
 
 // CTA-pair tiles (256 x 256) for BLOCK_N = 256 problems with K >= 768 and at
-// least one full wave of pair tiles; AFG_GEMM_PAIR=0 disables them (A/B).
+// least one full wave of pair tiles; AFG_GEMM_PAIR=0 disables them, =2 forces
+// them whenever K >= 768 (A/B knobs; 2048^3 forced: 24.1 vs 22.5 us).
 bool use_pair_tiles(int block_n, int64_t M, int64_t N, int64_t K) {
-  static const bool enabled = [] {
+  static const int mode = [] {  // 0 = off, 2 = whenever K >= 768 (A/B)
     const char* e = getenv("AFG_GEMM_PAIR");
-    return !(e && atoi(e) == 0);
+    return e ? atoi(e) : 1;
   }();
+  const bool enabled = mode != 0;
   // short K (<= 8 k-blocks) is epilogue / HBM bound: the pair's cross-CTA
   // accumulator hand-off costs more than the halved B staging saves
   // (measured: ResNet 1x1 convs and BERT K = 768 GEMMs)
   if (!enabled || block_n != 256 || M < 256 || K < 768) return false;
   const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  return pair_tiles >= num_sms() / 2;
+  return mode == 2 || pair_tiles >= num_sms() / 2;
 }
 
 // Four epilogue warp groups (640-thread CTA, one C staging buffer per group)
