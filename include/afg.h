@@ -24,6 +24,8 @@
  *   afg_layernorm_residual<- (no reference op; additive extension)
  *   afg_elementwise       <- lowerElementwiseBinary frontend.cpp:447-459, exp
  *   afg_reduce_lastdim    <- lowerReduceShaped      frontend.cpp:628-675
+ *   afg_gemm_i8           <- quant repositioning    SPEC.md:531-572 (quant.cpp
+ *                            is a stub): i8 x i8 -> i32 matmul + requant
  *
  * Conventions
  *  - All tensor pointers are caller-owned DEVICE pointers, dense row-major
@@ -211,6 +213,20 @@ AFG_API afg_status afg_reduce_lastdim(const void* x, void* out, int64_t rows, in
 AFG_API afg_status afg_broadcast_in_dim(const void* x, void* y, int in_rank, const int64_t* in_shape,
                                 int out_rank, const int64_t* out_shape, const int64_t* dims,
                                 afg_dtype x_dtype, afg_dtype y_dtype, void* stream);
+
+/* int8 GEMM (quant module: the repositioned
+ * dequant(Qa) . dequant(Qb) -> quant pattern; K1c, tcgen05 kind::i8).
+ * A: i8 [M,K] row-major (pitch lda bytes); B: i8 [N,K] row-major (K-major,
+ * pitch ldb bytes; the reference's [K,N] operand transposed once, e.g. with
+ * afg_transpose); exact i32 accumulation (K < 131072). out_mode:
+ *  0: C i32 [M,N] = A . B^T                     (bit-exact integer matmul)
+ *  1: C i8  = clamp(round_half_away(acc * scale), -128, 127)   (requantise)
+ *  2: C f32 = (float)(acc * scale)                            (dequantise)
+ * with scale = s_a * s_b (/ s_out for mode 1), applied in double. ldc in
+ * elements of C. A / B need 16-byte aligned bases and pitches. */
+AFG_API afg_status afg_gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                               int64_t ldc, int64_t M, int64_t N, int64_t K, int out_mode,
+                               float scale, void* stream);
 
 /* Quantisation chain (interp.cpp quant/dequant; oracles.cpp:387-398):
  *  mode 0 quantize  : y = clamp(round_half_away(x / scale), -128, 127)

@@ -168,6 +168,35 @@ def batch_matmul(A, B):
     return C
 
 
+# ------------------------------------------------------------- int8 GEMM ---
+
+def quantize(x, scale):
+    """The interpreter's `quant`: clamp(round_half_away(x / scale), -128, 127)
+    (test_interp.cpp:286-307 KAT; SPEC.md:531-572 QuantScheme)."""
+    y = np.asarray(x, dtype=np.float64) / np.float64(scale)
+    return np.clip(np.sign(y) * np.floor(np.abs(y) + 0.5), -128, 127)
+
+
+def matmul_i8(A, B_nk, mode=0, scale=1.0, rows=None):
+    """int8 x int8 -> int32 matmul as the reference evaluates an i8 matmul
+    graph (lowerMatmul nest, frontend.cpp:679-733; double arithmetic exact
+    for |sum| < 2^53, interp.cpp:502-561; I32 store = nearbyint + saturate,
+    interp.cpp:25-104), with B given as [N, K]. mode 1 requantises the
+    accumulator with round half away from zero and saturation (the `quant`
+    op), mode 2 dequantises to f32; scale is the f32 the C ABI receives,
+    applied in double."""
+    A = np.asarray(A, dtype=np.int64)
+    if rows is not None:
+        A = A[np.asarray(rows)]
+    acc = np.clip(A @ np.asarray(B_nk, dtype=np.int64).T, -2**31, 2**31 - 1)
+    if mode == 0:
+        return acc.astype(np.int32)
+    x = acc.astype(np.float64) * np.float64(np.float32(scale))
+    if mode == 1:
+        return np.clip(np.sign(x) * np.floor(np.abs(x) + 0.5), -128, 127).astype(np.int8)
+    return x.astype(np.float32)
+
+
 # ----------------------------------------------------------------- conv ---
 
 def conv_geometry(inH, inW, kH, kW, stride=(1, 1), dil=(1, 1), same=False, transposed=False):

@@ -1,0 +1,323 @@
+// K1c — int8 GEMM on the 5th-generation tensor cores (tcgen05 kind::i8).
+//
+// The quant module's repositioned form (PAPER.md Appendix
+// A.1): dequant(Qa) . dequant(Qb) -> quant becomes an i8 x i8 matmul with an
+// exact i32 accumulator and the combined scale applied once at the output.
+// Output modes (afg.h): the i32 accumulator itself (bit-exact vs the integer
+// oracle), a requantised i8 (round half away from zero, saturating — the
+// interpreter's `quant`, test_interp.cpp:286-307), or the dequantised f32.
+//
+// Structure (same pipeline as K1, gemm_tc.cu): persistent CTA per SM, warp 0
+// streams 128-byte K slabs of A [128 rows] and B [256 rows, K-major] with TMA
+// (128B swizzle) into a 4-deep ring, warp 1 issues 128 x 256 x 32 MMAs (one
+// elected lane, warp-uniform loop), warp 2 owns 512 TMEM columns (two
+// 256-column s32 accumulators: the epilogue of tile i overlaps the MMAs of
+// tile i+1), warps 4-7 read the accumulator rows back (one row per thread)
+// and store them. The scaling math runs in double, as the reference's
+// interpreter does (interp.cpp:502-561), so requantised / dequantised outputs
+// round exactly like the oracle.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "afg_internal.h"
+#include "sm100.cuh"
+
+namespace afg {
+namespace {
+
+using namespace sm100;
+
+constexpr int I8_BM = 128;
+constexpr int I8_BN = 256;
+constexpr int I8_BK = 128;  // K elements (= bytes) per stage: one 128-byte swizzle row
+constexpr int I8_STAGES = 4;
+
+struct I8Smem {
+  static constexpr int A_BYTES = I8_BM * I8_BK;
+  static constexpr int B_BYTES = I8_BN * I8_BK;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = I8_STAGES * STAGE_BYTES;
+  static constexpr int NUM_BARS = 2 * I8_STAGES + 4;
+  static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
+  static_assert(TOTAL <= 232448, "gemm_i8 smem");
+};
+
+struct I8Args {
+  int M, N, K;
+  int64_t ldc;  // elements of the output type
+  void* C;
+  int mode;  // 0 i32, 1 requantised i8, 2 dequantised f32
+  double scale;
+  int nmb, nnb;
+};
+
+// tcgen05 instruction descriptor, kind::i8: D = s32, A = B = signed 8-bit,
+// both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8_if(bool leader, uint32_t tmem_d, uint64_t adesc,
+                                          uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(static_cast<uint32_t>(leader))
+      : "memory");
+}
+
+// round half away from zero, saturate to [-128, 127] (interp quant)
+__device__ __forceinline__ int requant_i8(int acc, double scale) {
+  const double r = round(static_cast<double>(acc) * scale);
+  return static_cast<int>(fmin(fmax(r, -128.0), 127.0));
+}
+
+__device__ __forceinline__ void store_row32(const uint32_t (&r)[32], const I8Args& a, int row,
+                                            int col0) {
+  if (row >= a.M || col0 >= a.N) return;
+  const bool full = col0 + 32 <= a.N;
+  if (a.mode == 0) {
+    int32_t* dst = static_cast<int32_t*>(a.C) + static_cast<int64_t>(row) * a.ldc + col0;
+    if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < a.N) dst[j] = static_cast<int32_t>(r[j]);
+    }
+  } else if (a.mode == 1) {
+    int8_t* dst = static_cast<int8_t*>(a.C) + static_cast<int64_t>(row) * a.ldc + col0;
+    uint32_t w[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        x |= (static_cast<uint32_t>(requant_i8(static_cast<int>(r[4 * v + b]), a.scale)) & 0xffu)
+             << (8 * b);
+      w[v] = x;
+    }
+    if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < a.N) dst[j] = static_cast<int8_t>((w[j / 4] >> (8 * (j % 4))) & 0xffu);
+    }
+  } else {
+    float* dst = static_cast<float*>(a.C) + static_cast<int64_t>(row) * a.ldc + col0;
+    float f[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      f[j] = static_cast<float>(static_cast<double>(static_cast<int>(r[j])) * a.scale);
+    if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        reinterpret_cast<float4*>(dst)[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < a.N) dst[j] = f[j];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const I8Args args) {
+  using L = I8Smem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + I8_STAGES;
+  uint64_t* tfull_bar = bars + 2 * I8_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < I8_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  griddep_launch_dependents();
+
+  const int num_tiles = args.nmb * args.nnb;
+  const int num_kb = (args.K + I8_BK - 1) / I8_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t % args.nmb) * I8_BM;
+        const int n0 = (t / args.nmb) * I8_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], L::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full_bar[stage], kb * I8_BK, m0);
+          tma_load_2d(sa + L::A_BYTES, &tmB, &full_bar[stage], kb * I8_BK, n0);
+          if (++stage == I8_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_i8(I8_BM, I8_BN);
+    const uint64_t a_desc0 = desc_kmajor_sw128(smem_u32(smem));
+    const uint64_t b_desc0 = desc_kmajor_sw128(smem_u32(smem + L::A_BYTES));
+    constexpr uint64_t STAGE_STEP = L::STAGE_BYTES >> 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    int iter = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      const int acc = iter & 1;
+      mbar_wait(&tempty_bar[acc], ((iter >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * I8_BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
+        const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
+#pragma unroll
+        for (int k = 0; k < I8_BK / 32; ++k)  // 32 bytes of K per MMA
+          mma_i8_if(leader, d_tmem, ad + static_cast<uint64_t>((k * 32) >> 4),
+                    bd + static_cast<uint64_t>((k * 32) >> 4), idesc, (kb | k) != 0 ? 1u : 0u);
+        mma_commit_if(leader, &empty_bar[stage]);
+        if (++stage == I8_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      mma_commit_if(leader, &tfull_bar[acc]);
+    }
+  } else if (warp >= 4) {
+    const int ew = warp % 4;
+    const int rloc = ew * 32 + lane;
+    int iter = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+      const int acc = iter & 1;
+      mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
+      tc_fence_after();
+      const int row = (t % args.nmb) * I8_BM + rloc;
+      const int n0 = (t / args.nmb) * I8_BN;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * I8_BN;
+#pragma unroll 1
+      for (int c = 0; c < I8_BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(t_row + c * 32, r);
+        tmem_wait_ld();
+        if (c == I8_BN / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty_bar[acc]);
+        }
+        store_row32(r, args, row, n0 + c * 32);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace
+
+afg_status gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                   int64_t M, int64_t N, int64_t K, int mode, double scale, cudaStream_t stream) {
+  CUtensorMap tmA, tmB;
+  afg_status st = make_tmap_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, M, lda, I8_BK, I8_BM);
+  if (st != AFG_OK) return st;
+  st = make_tmap_2d(&tmB, B, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, ldb, I8_BK, I8_BN);
+  if (st != AFG_OK) return st;
+  I8Args a;
+  a.M = static_cast<int>(M);
+  a.N = static_cast<int>(N);
+  a.K = static_cast<int>(K);
+  a.ldc = ldc;
+  a.C = C;
+  a.mode = mode;
+  a.scale = scale;
+  a.nmb = static_cast<int>((M + I8_BM - 1) / I8_BM);
+  a.nnb = static_cast<int>((N + I8_BN - 1) / I8_BN);
+  constexpr int smem = I8Smem::TOTAL;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_status(e, "gemm_i8 smem attribute");
+    configured = true;
+  }
+  const int tiles = a.nmb * a.nnb;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min(tiles, num_sms())));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel, tmA, tmB, a);
+  count_launch();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return cuda_status(e, "gemm_i8 launch");
+}
+
+}  // namespace afg
+
+using namespace afg;
+
+extern "C" afg_status afg_gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                                  int64_t ldc, int64_t M, int64_t N, int64_t K, int out_mode,
+                                  float scale, void* stream) {
+  if (!A || !B || !C) return set_error(AFG_ERR_INVALID_ARG, "afg_gemm_i8: null operand");
+  if (M <= 0 || N <= 0 || K <= 0 || M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 17))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_gemm_i8: extent out of range (K < 131072 keeps i32 exact)");
+  if (out_mode < 0 || out_mode > 2)
+    return set_error(AFG_ERR_INVALID_ARG, "afg_gemm_i8: bad out_mode %d", out_mode);
+  if (out_mode != 0 && !(scale > 0.0f))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_gemm_i8: scale must be positive");
+  if (lda < K || ldb < K || ldc < N)
+    return set_error(AFG_ERR_INVALID_ARG, "afg_gemm_i8: leading dimension too small");
+  if (lda % 16 != 0 || ldb % 16 != 0 || !aligned16(A) || !aligned16(B))
+    return set_error(AFG_ERR_UNSUPPORTED,
+                     "afg_gemm_i8: A / B need 16-byte aligned bases and row pitches (TMA)");
+  afg_status st = check_device();
+  if (st != AFG_OK) return st;
+  return gemm_i8(A, lda, B, ldb, C, ldc, M, N, K, out_mode, static_cast<double>(scale),
+                 static_cast<cudaStream_t>(stream));
+}

@@ -53,6 +53,23 @@ def gemm(a, b, bias=None, epilogue=Epilogue.NONE, out_dtype=None, b_layout=Layou
     return out
 
 
+def gemm_i8(a, b_nk, out_mode=0, scale=1.0, out=None):
+    """int8 GEMM on tcgen05 kind::i8 (quant repositioning, SPEC.md:531-572).
+    a int8 [M,K], b_nk int8 [N,K]; out_mode 0 -> int32 A.B^T (exact),
+    1 -> int8 requantised clamp(round_half_away(acc*scale)), 2 -> float32 acc*scale."""
+    _need_cuda(a, b_nk, out)
+    if a.dtype != torch.int8 or b_nk.dtype != torch.int8:
+        raise AfgError(1, "gemm_i8 takes int8 operands")
+    M, K = a.shape
+    N = b_nk.shape[0]
+    od = {0: torch.int32, 1: torch.int8, 2: torch.float32}[int(out_mode)]
+    if out is None:
+        out = torch.empty((M, N), dtype=od, device=a.device)
+    check(lib().afg_gemm_i8(_ptr(a), a.stride(0), _ptr(b_nk), b_nk.stride(0), _ptr(out),
+                            out.stride(0), M, N, K, int(out_mode), float(scale), _stream()))
+    return out
+
+
 def gemm_batched(a, b, out_dtype=None):
     _need_cuda(a, b)
     *bd, M, K = a.shape

@@ -1,0 +1,75 @@
+"""GPU parity of K1c (int8 GEMM, tcgen05 kind::i8; the quant module's
+repositioned matmul) against the integer oracle
+(oracle.matmul_i8) and the reference interpreter's own outputs
+(tests/golden/int8_matmul.json). Integer work: bit-exact, tolerance 0 —
+including the requantised i8 (round half away from zero, saturating) and the
+dequantised f32 (acc * scale in double, rounded once to f32)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2603_06731_b200 import AfgError, ops
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def i8(shape, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(-128, 128, shape, generator=g, dtype=torch.int8)
+
+
+def test_reference_fixtures_bit_exact(cuda):
+    for c in json.load(open(os.path.join(GOLD, "int8_matmul.json")))["cases"]:
+        a = np.array(c["a"], dtype=np.int8)
+        b = np.array(c["b"], dtype=np.int8)
+        K = a.shape[1]
+        Kp = (K + 15) // 16 * 16  # TMA row pitch: 16 bytes
+        ad = torch.zeros((a.shape[0], Kp), dtype=torch.int8)
+        ad[:, :K] = torch.from_numpy(a)
+        bd = torch.zeros((b.shape[1], Kp), dtype=torch.int8)
+        bd[:, :K] = torch.from_numpy(np.ascontiguousarray(b.T))
+        got = ops.gemm_i8(ad.cuda()[:, :K], bd.cuda()[:, :K]).cpu().numpy()
+        assert np.array_equal(got, np.array(c["c"])), c["name"]
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (333, 200, 144), (1000, 520, 1040),
+                                   (64, 64, 16), (2048, 1024, 4096)])
+def test_i32_exact(cuda, M, N, K):
+    a, b = i8((M, K), M), i8((N, K), N + 1)
+    got = ops.gemm_i8(a.cuda(), b.cuda()).cpu().numpy()
+    rows = None if M * N * K <= 2**28 else np.r_[0:3, M // 2, M - 1]
+    want = O.matmul_i8(a.numpy(), b.numpy(), rows=rows)
+    assert np.array_equal(got if rows is None else got[rows], want)
+
+
+@pytest.mark.parametrize("mode,scale", [(1, 1 / 4096), (1, 0.5), (2, 3.1e-5)])
+def test_requant_and_dequant(cuda, mode, scale):
+    M, N, K = 300, 384, 512
+    a, b = i8((M, K), 5), i8((N, K), 6)
+    got = ops.gemm_i8(a.cuda(), b.cuda(), out_mode=mode, scale=scale).cpu().numpy()
+    want = O.matmul_i8(a.numpy(), b.numpy(), mode=mode, scale=scale)
+    assert np.array_equal(got, want)
+    if mode == 1 and scale == 0.5:  # saturates both ways
+        assert (got == 127).any() and (got == -128).any()
+
+
+def test_many_tiles_per_cta(cuda):
+    """>= 3 tiles per persistent CTA (TMEM accumulator double-buffer phases)."""
+    M, N, K = 148 * 128 * 3 + 50, 256, 256
+    a, b = i8((M, K), 9), i8((N, K), 10)
+    got = ops.gemm_i8(a.cuda(), b.cuda()).cpu().numpy()
+    rows = np.arange(0, M, 997)
+    assert np.array_equal(got[rows], O.matmul_i8(a.numpy(), b.numpy(), rows=rows))
+
+
+def test_rejects_unaligned_pitch(cuda):
+    a = torch.zeros((8, 20), dtype=torch.int8, device="cuda")
+    b = torch.zeros((8, 20), dtype=torch.int8, device="cuda")
+    with pytest.raises(AfgError):
+        ops.gemm_i8(a, b)

@@ -204,3 +204,41 @@ def test_live_reference_reproduces_committed_fixtures():
         out = O.ref_run(json.dumps(c["graph"]), ins, "interpret")
         for k, v in c["interpret"].items():
             assert np.array_equal(out[k], dec(v)), (c["name"], k)
+
+
+# ------------------------------------------------------------- int8 path ---
+
+I8 = json.load(open(os.path.join(GOLD, "int8_matmul.json")))["cases"]
+
+
+def test_quantize_kat():
+    # test_interp.cpp:286-307: quant scale 0.5 -> {1, -2, 127, -1}
+    assert O.quantize([0.74, -0.76, 100.0, -0.25], 0.5).tolist() == [1, -2, 127, -1]
+
+
+def test_int8_matmul_restatement_vs_reference_fixtures():
+    for c in I8:
+        a, b = np.array(c["a"]), np.array(c["b"])
+        got = O.matmul_i8(a, b.T)
+        assert np.array_equal(got, np.array(c["c"])), c["name"]
+
+
+def test_int8_requant_rounding_half_away():
+    acc_a = np.array([[1, 1, 1]])
+    b = np.array([[1, 0, 0], [1, 1, 1], [-1, -1, -1]])  # acc = 1, 3, -3
+    got = O.matmul_i8(acc_a, b, mode=1, scale=0.5)  # 0.5 -> 1, 1.5 -> 2, -1.5 -> -2
+    assert got.tolist() == [[1, 2, -2]]
+    assert O.matmul_i8(np.full((1, 64), 127), np.full((1, 64), 127), mode=1, scale=1.0).tolist() == [[127]]
+
+
+@needs_ref
+def test_int8_matmul_restatement_vs_live_reference():
+    rng = np.random.default_rng(7)
+    M, K, N = 9, 72, 11
+    a, b = rng.integers(-128, 128, (M, K)), rng.integers(-128, 128, (K, N))
+    g = {"tensors": [{"id": "a", "shape": [M, K], "dtype": "i8"},
+                     {"id": "b", "shape": [K, N], "dtype": "i8"},
+                     {"id": "c", "shape": [M, N], "dtype": "i32"}],
+         "ops": [{"op": "matmul", "inputs": ["a", "b"], "output": "c"}]}
+    out = O.ref_run(json.dumps(g), {"a": a, "b": b}, "interpret")["%c"]
+    assert np.array_equal(O.matmul_i8(a, b.T), out)
