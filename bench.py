@@ -234,6 +234,68 @@ class GemmBF16:
         return ReferenceGemmSample(self.n, threads)
 
 
+class GemmI8:
+    """SURVEY 8f3 (beyond the BASELINE configs): the quant module's int8 GEMM
+    (SPEC.md:531-572), i8 x i8 -> exact i32 accumulation, requantised to i8
+    (round half away from zero, saturating), tcgen05 kind::i8."""
+
+    metric = "TOP/s"
+    unit = "TOP/s"
+    dtype = "int8"
+    bound = "tensor-i8"
+
+    def __init__(self, size):
+        self.n = size
+        self.name = f"gemm_i8_{size}"
+
+    def config(self, world):
+        return {"workload": f"int8 matmul {self.n}x{self.n}x{self.n}, i32 accumulate, requantised "
+                            f"i8 output (scale 2^-12), row-sharded",
+                "M": self.n, "N": self.n, "K": self.n, "parallelism": f"rows/{world}",
+                "l2": "operands larger than L2 (no flush needed)"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        from paper_2603_06731_b200 import ops
+        self.torch, self.ops = torch, ops
+        r0, r1 = shard_rows(self.n, rank, world)
+        self.m = r1 - r0
+        g = torch.Generator(device=dev).manual_seed(1000 + r0)
+        self.A = torch.randint(-128, 128, (self.m, self.n), generator=g, dtype=torch.int8, device=dev)
+        g.manual_seed(2)
+        self.B = torch.randint(-128, 128, (self.n, self.n), generator=g, dtype=torch.int8, device=dev)
+        self.C = torch.empty((self.m, self.n), dtype=torch.int8, device=dev)
+        self.flops_rank = 2.0 * self.m * self.n * self.n
+        self.flops_total = 2.0 * self.n ** 3
+        self.alg_bytes_rank = float(self.m * self.n + self.n * self.n + self.m * self.n)
+
+    def step(self):
+        self.ops.gemm_i8(self.A, self.B, out_mode=1, scale=2.0 ** -12, out=self.C)
+
+    def launches_per_step(self):
+        return 1
+
+    def e2e_setup(self):
+        t = self.torch
+        self.hA = self.A.cpu().pin_memory()
+        self.hB = self.B.cpu().pin_memory()
+        self.hC = t.empty((self.m, self.n), dtype=t.int8).pin_memory()
+        self.dA = t.empty_like(self.A)
+        self.dB = t.empty_like(self.B)
+        self.h2d = self.hA.numel() + self.hB.numel()
+        self.d2h = self.hC.numel()
+
+    def e2e_step(self):
+        self.dA.copy_(self.hA, non_blocking=True)
+        self.dB.copy_(self.hB, non_blocking=True)
+        self.ops.gemm_i8(self.dA, self.dB, out_mode=1, scale=2.0 ** -12, out=self.C)
+        self.hC.copy_(self.C, non_blocking=True)
+
+    def reference_sample(self, threads):
+        return ReferenceI8Sample(self.n, threads)
+
+
 class GemmFP32:
     """BASELINE configs[0]: fp32 1024^3 + bias + ReLU (replicas only)."""
 
@@ -600,6 +662,7 @@ class MemChain(_Base):
 
 
 WORKLOADS = {"gemm_bf16": lambda a: GemmBF16(a.size), "gemm_fp32": lambda a: GemmFP32(),
+             "gemm_i8": lambda a: GemmI8(a.size),
              "attention": lambda a: Attention(False), "attention_causal": lambda a: Attention(True),
              "resnet50_convs": lambda a: ResNetConvs(), "bert_layer": lambda a: BertLayer(),
              "softmax": lambda a: MemChain("softmax"), "layernorm": lambda a: MemChain("layernorm")}
@@ -652,6 +715,46 @@ class ReferenceGemmSample:
                 ins = {k: O.round_to(v, O.F32) for k, v in self.inputs.items()}
                 epi = O.EPI_GELU_TANH if self.act == "gelu" else O.EPI_RELU
                 O.matmul(ins["a"], ins["b"], ins["bias"], epi=epi, interp=True, nthreads=1)
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            list(ex.map(one, range(self.threads)))
+        return time.perf_counter() - t0
+
+
+class ReferenceI8Sample:
+    """Bounded reference-path sample of the int8 GEMM: one af::interpret
+    instance per host thread on an i8 [rows x K] x [K x cols] -> i32 matmul
+    graph (the oracle's integer restatement when oracle/_ref is absent)."""
+
+    def __init__(self, K, threads, rows=2, cols=32):
+        import oracle as O
+        self.O, self.K, self.threads, self.rows, self.cols = O, K, threads, rows, cols
+        self.kind = "reference" if O.ref_available() else "port"
+        rng = np.random.default_rng(7)
+        self.a = rng.integers(-128, 128, (rows, K))
+        self.b = rng.integers(-128, 128, (K, cols))
+        self.graph = json.dumps({
+            "tensors": [{"id": "a", "shape": [rows, K], "dtype": "i8"},
+                        {"id": "b", "shape": [K, cols], "dtype": "i8"},
+                        {"id": "c", "shape": [rows, cols], "dtype": "i32"}],
+            "ops": [{"op": "matmul", "inputs": ["a", "b"], "output": "c"}]})
+        self.flops = 2.0 * rows * cols * K * threads
+
+    def describe(self):
+        how = "af::interpret (oracle/_ref)" if self.kind == "reference" else "oracle integer port"
+        return (f"{self.threads} independent shards of i8 [{self.rows}x{self.K}]x[{self.K}x"
+                f"{self.cols}] -> i32 matmul via {how}")
+
+    def run_once(self):
+        from concurrent.futures import ThreadPoolExecutor
+        O = self.O
+
+        def one(_):
+            if self.kind == "reference":
+                O.ref_run(self.graph, {"a": self.a, "b": self.b}, "interpret")
+            else:
+                O.matmul_i8(self.a, self.b.T)
 
         t0 = time.perf_counter()
         with ThreadPoolExecutor(self.threads) as ex:
@@ -841,9 +944,14 @@ def run_afg(args, wl, rank, world, local):
     # roofline of the step's kernels on this rank (device time of the step;
     # single-kernel workloads: exactly the dominant kernel's duration)
     k_ms = statistics.median(step_ms)
+    peak_note = f"{peaks['source']} (MEASURED_PEAKS.json burst)"
     if wl.bound == "hbm":
         achieved = wl.alg_bytes_rank / (k_ms * 1e-3) / 1e9
         peak, unit = peaks["hbm_gbs"], "GB/s"
+    elif wl.bound == "tensor-i8":  # dense int8 = 2x dense bf16 on B200 (4.5 vs 2.25 PFLOP/s nominal)
+        achieved = wl.flops_rank / (k_ms * 1e-3) / 1e12
+        peak, unit = 2.0 * peaks["bf16_tflops"], "TOP/s"
+        peak_note = f"2 x the {peaks['source']} bf16 burst peak (MEASURED_PEAKS.json has no int8 entry)"
     else:
         achieved = wl.flops_rank / (k_ms * 1e-3) / 1e12
         peak, unit = peaks["bf16_tflops"], "TFLOP/s"
@@ -885,7 +993,7 @@ def run_afg(args, wl, rank, world, local):
                 "roofline": {"bound": wl.bound if wl.bound in ("hbm", "tensor") else "tensor",
                              "achieved": achieved, "peak": peak, "unit": unit,
                              "frac": achieved / peak,
-                             "peak_source": f"{peaks['source']} (MEASURED_PEAKS.json burst)",
+                             "peak_source": peak_note,
                              "kernel_ms": k_ms, "traffic": traffic_for(wl.name),
                              **floor_fields(wl, peaks, k_ms)},
                 "e2e": {"value": e2e_value, "unit": wl.unit, "ms_per_step": e_ms,

@@ -7,7 +7,7 @@ mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $O/smi.txt 2>&1
 timeout -s KILL 1200 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -5 > $O/pytest_gpu.log
 timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
-for w in gemm_bf16 gemm_fp32 attention attention_causal resnet50_convs bert_layer softmax layernorm; do
+for w in gemm_bf16 gemm_fp32 gemm_i8 attention attention_causal resnet50_convs bert_layer softmax layernorm; do
   timeout -s KILL 300 python bench.py --workload $w --steps 10 --warmup 3 > $O/bench_$w.json 2> $O/bench_$w.err
 done
 for n in 2048 4096 8192; do
@@ -15,7 +15,7 @@ for n in 2048 4096 8192; do
 done
 timeout -s KILL 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference.json 2>&1
 # launch lists (cold-cache, serialised: shares, not absolutes)
-for w in gemm_bf16 attention attention_causal resnet50_convs bert_layer softmax layernorm gemm_fp32; do
+for w in gemm_bf16 gemm_i8 attention attention_causal resnet50_convs bert_layer softmax layernorm gemm_fp32; do
   timeout -s KILL 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$w.csv \
     python bench.py --workload $w --steps 1 --warmup 3 --no-cpu-baseline --no-graph > /dev/null 2>&1
 done
@@ -39,4 +39,5 @@ cap resnet50_convs conv_halo resnet_conv_halo
 cap resnet50_convs gemm_tc resnet_conv_gemm
 cap bert_layer attn_fwd bert_attention
 cap gemm_fp32 gemm_simt gemm_fp32
+cap gemm_i8 gemm_i8 gemm_i8_16384
 echo done > $O/done
