@@ -10,10 +10,11 @@
 // Structure (same pipeline as K1, gemm_tc.cu): persistent CTA per SM, warp 0
 // streams 128-byte K slabs of A [128 rows] and B [256 rows, K-major] with TMA
 // (128B swizzle) into a 4-deep ring, warp 1 issues 128 x 256 x 32 MMAs (one
-// elected lane, warp-uniform loop), warp 2 owns 512 TMEM columns (two
+// elected lane, warp-uniform loop; 256 x 256 x 32 on a CTA pair with a 6-deep
+// ring of half-B stages when the tiles fill the GPU), warp 2 owns 512 TMEM columns (two
 // 256-column s32 accumulators: the epilogue of tile i overlaps the MMAs of
-// tile i+1), warps 4-7 read the accumulator rows back (one row per thread)
-// and store them. The scaling math runs in double, as the reference's
+// tile i+1), warps 4-11 (two warpgroups, alternate 32-column chunks) read the
+// accumulator rows back (one row per thread) and store them. The scaling math runs in double, as the reference's
 // interpreter does (interp.cpp:502-561), so requantised / dequantised outputs
 // round exactly like the oracle.
 #include <cuda.h>
@@ -21,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "afg_internal.h"
 #include "sm100.cuh"
@@ -33,14 +35,18 @@ using namespace sm100;
 constexpr int I8_BM = 128;
 constexpr int I8_BN = 256;
 constexpr int I8_BK = 128;  // K elements (= bytes) per stage: one 128-byte swizzle row
-constexpr int I8_STAGES = 4;
-
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x 256 tile
+// with one M = 256 MMA per K step; each CTA stages its 128 rows of A and half
+// of B (as K1's pair tiles): half the B bytes per SM in smem and L2.
+template <bool PAIR>
 struct I8Smem {
+  static constexpr int STAGES = PAIR ? 6 : 4;
+  static constexpr int B_ROWS = PAIR ? I8_BN / 2 : I8_BN;
   static constexpr int A_BYTES = I8_BM * I8_BK;
-  static constexpr int B_BYTES = I8_BN * I8_BK;
+  static constexpr int B_BYTES = B_ROWS * I8_BK;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = I8_STAGES * STAGE_BYTES;
-  static constexpr int NUM_BARS = 2 * I8_STAGES + 4;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
   static_assert(TOTAL <= 232448, "gemm_i8 smem");
 };
@@ -60,14 +66,16 @@ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+template <int CG>
 __device__ __forceinline__ void mma_i8_if(bool leader, uint32_t tmem_d, uint64_t adesc,
                                           uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p, q;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "setp.ne.b32 q, %5, 0;\n\t"
-      "@q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(static_cast<uint32_t>(leader))
+      "@q tcgen05.mma.cta_group::%6.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(static_cast<uint32_t>(leader)),
+      "n"(CG)
       : "memory");
 }
 
@@ -130,38 +138,49 @@ __device__ __forceinline__ void store_row32(const uint32_t (&r)[32], const I8Arg
   }
 }
 
-__global__ void __launch_bounds__(256, 1)
+template <bool PAIR>
+__global__ void __launch_bounds__(384, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const I8Args args) {
-  using L = I8Smem;
+  using L = I8Smem<PAIR>;
+  constexpr int NS = L::STAGES;
+  constexpr int TILE_M = PAIR ? 2 * I8_BM : I8_BM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* full_bar = bars;
-  uint64_t* empty_bar = bars + I8_STAGES;
-  uint64_t* tfull_bar = bars + 2 * I8_STAGES;
+  uint64_t* empty_bar = bars + NS;
+  uint64_t* tfull_bar = bars + 2 * NS;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int cid = PAIR ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int ncl = PAIR ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < I8_STAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      // PAIR: one arrival per epilogue warp of both CTAs (on the leader's)
+      mbar_init(&tempty_bar[s], PAIR ? 16 : 256);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();
@@ -174,16 +193,23 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t % args.nmb) * I8_BM;
-        const int n0 = (t / args.nmb) * I8_BN;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        const int m0 = (t % args.nmb) * TILE_M + static_cast<int>(rank) * I8_BM;
+        const int n0 = (t / args.nmb) * I8_BN + static_cast<int>(rank) * L::B_ROWS;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], L::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full_bar[stage], kb * I8_BK, m0);
-          tma_load_2d(sa + L::A_BYTES, &tmB, &full_bar[stage], kb * I8_BK, n0);
-          if (++stage == I8_STAGES) {
+          // PAIR: both CTAs' bytes complete on the leader's full barrier
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], (PAIR ? 2 : 1) * L::STAGE_BYTES);
+          if constexpr (PAIR) {
+            const uint32_t fb = mapa_shared(&full_bar[stage], 0);
+            tma_load_2d_pair(sa, &tmA, fb, kb * I8_BK, m0);
+            tma_load_2d_pair(sa + L::A_BYTES, &tmB, fb, kb * I8_BK, n0);
+          } else {
+            tma_load_2d(sa, &tmA, &full_bar[stage], kb * I8_BK, m0);
+            tma_load_2d(sa + L::A_BYTES, &tmB, &full_bar[stage], kb * I8_BK, n0);
+          }
+          if (++stage == NS) {
             stage = 0;
             phase ^= 1;
           }
@@ -191,76 +217,142 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_i8(I8_BM, I8_BN);
-    const uint64_t a_desc0 = desc_kmajor_sw128(smem_u32(smem));
-    const uint64_t b_desc0 = desc_kmajor_sw128(smem_u32(smem + L::A_BYTES));
-    constexpr uint64_t STAGE_STEP = L::STAGE_BYTES >> 4;
-    int stage = 0;
-    uint32_t phase = 0;
-    int iter = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
-      const int acc = iter & 1;
-      mbar_wait(&tempty_bar[acc], ((iter >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * I8_BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+    if (rank == 0) {  // PAIR: the leader CTA issues for both
+      const bool leader = elect_one();
+      constexpr uint32_t idesc = idesc_i8(TILE_M, I8_BN);
+      const uint64_t a_desc0 = desc_kmajor_sw128(smem_u32(smem));
+      const uint64_t b_desc0 = desc_kmajor_sw128(smem_u32(smem + L::A_BYTES));
+      constexpr uint64_t STAGE_STEP = L::STAGE_BYTES >> 4;
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int t = cid; t < num_tiles; t += ncl, ++iter) {
+        const int acc = iter & 1;
+        if constexpr (PAIR) mbar_wait_cluster(&tempty_bar[acc], ((iter >> 1) & 1) ^ 1);
+        else mbar_wait(&tempty_bar[acc], ((iter >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
-        const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
+        const uint32_t d_tmem = tmem_base + acc * I8_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage) * STAGE_STEP;
 #pragma unroll
-        for (int k = 0; k < I8_BK / 32; ++k)  // 32 bytes of K per MMA
-          mma_i8_if(leader, d_tmem, ad + static_cast<uint64_t>((k * 32) >> 4),
-                    bd + static_cast<uint64_t>((k * 32) >> 4), idesc, (kb | k) != 0 ? 1u : 0u);
-        mma_commit_if(leader, &empty_bar[stage]);
-        if (++stage == I8_STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int k = 0; k < I8_BK / 32; ++k)  // 32 bytes of K per MMA
+            mma_i8_if<PAIR ? 2 : 1>(leader, d_tmem, ad + static_cast<uint64_t>((k * 32) >> 4),
+                                    bd + static_cast<uint64_t>((k * 32) >> 4), idesc,
+                                    (kb | k) != 0 ? 1u : 0u);
+          if constexpr (PAIR) mma_commit_pair_if(leader, &empty_bar[stage], 3);
+          else mma_commit_if(leader, &empty_bar[stage]);
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        if constexpr (PAIR) mma_commit_pair_if(leader, &tfull_bar[acc], 3);
+        else mma_commit_if(leader, &tfull_bar[acc]);
       }
-      mma_commit_if(leader, &tfull_bar[acc]);
     }
   } else if (warp >= 4) {
+    // two epilogue warpgroups (warps 4-7, 8-11) take alternate 32-column chunks
+    const int eg = (warp - 4) / 4;
     const int ew = warp % 4;
     const int rloc = ew * 32 + lane;
     int iter = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++iter) {
+    for (int t = cid; t < num_tiles; t += ncl, ++iter) {
       const int acc = iter & 1;
       mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
       tc_fence_after();
-      const int row = (t % args.nmb) * I8_BM + rloc;
+      const int row = (t % args.nmb) * TILE_M + static_cast<int>(rank) * I8_BM + rloc;
       const int n0 = (t / args.nmb) * I8_BN;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * I8_BN;
 #pragma unroll 1
-      for (int c = 0; c < I8_BN / 32; ++c) {
+      for (int c = eg; c < I8_BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld32(t_row + c * 32, r);
         tmem_wait_ld();
-        if (c == I8_BN / 32 - 1) {
+        if (c + 2 >= I8_BN / 32) {  // last TMEM read of the tile: release the accumulator
           tc_fence_before();
-          mbar_arrive(&tempty_bar[acc]);
+          if constexpr (PAIR) {
+            __syncwarp();
+            if (lane == 0) {
+              if (rank == 0) mbar_arrive(&tempty_bar[acc]);
+              else mbar_arrive_cluster(&tempty_bar[acc], 0);
+            }
+          } else {
+            mbar_arrive(&tempty_bar[acc]);
+          }
         }
         store_row32(r, args, row, n0 + c * 32);
       }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the leader's MMAs into the peer's TMEM are done
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
+}
+
+template <bool PAIR>
+cudaError_t launch_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const I8Args& a,
+                      cudaStream_t stream) {
+  constexpr int smem = I8Smem<PAIR>::TOTAL;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<PAIR>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int tiles = a.nmb * a.nnb;
+  const int grid = PAIR ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (PAIR) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<PAIR>, tmA, tmB, a);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
 
 afg_status gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                    int64_t M, int64_t N, int64_t K, int mode, double scale, cudaStream_t stream) {
+  // 256 x 256 tiles on CTA pairs when they fill at least half the SMs' pairs
+  // (AFG_GEMM_I8_PAIR=0 keeps single-CTA 128 x 256 tiles)
+  static const bool pair_env = [] {
+    const char* e = getenv("AFG_GEMM_I8_PAIR");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool pair = pair_env && M >= 256 && N >= 256 &&
+                    ((M + 255) / 256) * ((N + 255) / 256) >= num_sms() / 2;
   CUtensorMap tmA, tmB;
   afg_status st = make_tmap_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, M, lda, I8_BK, I8_BM);
   if (st != AFG_OK) return st;
-  st = make_tmap_2d(&tmB, B, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, ldb, I8_BK, I8_BN);
+  st = make_tmap_2d(&tmB, B, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, K, N, ldb, I8_BK,
+                    pair ? I8_BN / 2 : I8_BN);
   if (st != AFG_OK) return st;
   I8Args a;
   a.M = static_cast<int>(M);
@@ -270,30 +362,9 @@ afg_status gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void*
   a.C = C;
   a.mode = mode;
   a.scale = scale;
-  a.nmb = static_cast<int>((M + I8_BM - 1) / I8_BM);
+  a.nmb = static_cast<int>((M + (pair ? 2 : 1) * I8_BM - 1) / ((pair ? 2 : 1) * I8_BM));
   a.nnb = static_cast<int>((N + I8_BN - 1) / I8_BN);
-  constexpr int smem = I8Smem::TOTAL;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_status(e, "gemm_i8 smem attribute");
-    configured = true;
-  }
-  const int tiles = a.nmb * a.nnb;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::min(tiles, num_sms())));
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel, tmA, tmB, a);
-  count_launch();
-  if (e == cudaSuccess) e = cudaGetLastError();
+  const cudaError_t e = pair ? launch_i8<true>(tmA, tmB, a, stream) : launch_i8<false>(tmA, tmB, a, stream);
   return cuda_status(e, "gemm_i8 launch");
 }
 

@@ -1,5 +1,4 @@
-timeout 300 python bench.py --workload gemm_i8 --size 8192 --steps 10 --warmup 3 > gpurun_out/bench_gemm_i8_8192.json 2> gpurun_out/bench_gemm_i8.err
-timeout 300 python bench.py --workload gemm_i8 --steps 10 --warmup 3 > gpurun_out/bench_gemm_i8.json 2>> gpurun_out/bench_gemm_i8.err
-timeout 300 python bench.py --workload gemm_i8 --impl reference --steps 2 --warmup 1 > gpurun_out/bench_gemm_i8_reference.json 2>> gpurun_out/bench_gemm_i8.err
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_gemm_i8.csv python bench.py --workload gemm_i8 --steps 1 --warmup 3 --no-cpu-baseline --no-graph > /dev/null 2>&1
-cat gpurun_out/bench_gemm_i8_8192.json gpurun_out/bench_gemm_i8.json gpurun_out/bench_gemm_i8_reference.json | cut -c1-600; tail -3 gpurun_out/bench_gemm_i8.err
+timeout 300 python -m pytest tests/test_gemm_i8_gpu.py -m gpu -q -p no:cacheprovider 2>&1 | tail -3
+for p in 1 0; do for n in 16384 8192; do
+AFG_GEMM_I8_PAIR=$p timeout 300 python bench.py --workload gemm_i8 --size $n --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python3 -c "import json,sys;d=json.loads(sys.stdin.read());print('PAIR=$p n=$n', round(d['value'],1), round(d['ms_per_step'],3), 'ms', d['clocks']['sm_mhz'], d['clocks']['reasons'], d['roofline']['frac'])"
+done; done

@@ -73,3 +73,23 @@ def test_rejects_unaligned_pitch(cuda):
     b = torch.zeros((8, 20), dtype=torch.int8, device="cuda")
     with pytest.raises(AfgError):
         ops.gemm_i8(a, b)
+
+
+# 256 x 256 tiles on a CTA pair (cta_group::2 kind::i8) once there are >= 74 of
+# them: ragged M / N / K, every output mode, and >= 3 pair tiles per cluster.
+@pytest.mark.parametrize("mode,scale", [(0, 1.0), (1, 1 / 2048), (2, 1e-3)])
+def test_pair_tiles_ragged(cuda, mode, scale):
+    M, N, K = 2500, 2000, 208
+    a, b = i8((M, K), 11), i8((N, K), 12)
+    got = ops.gemm_i8(a.cuda(), b.cuda(), out_mode=mode, scale=scale).cpu().numpy()
+    rows = np.r_[0:2, 127:130, 255:258, 1024, 2047, 2300, M - 1]
+    assert np.array_equal(got[rows], O.matmul_i8(a.numpy(), b.numpy(), mode=mode, scale=scale,
+                                                 rows=rows))
+
+
+def test_pair_tiles_long_k_many_per_cluster(cuda):
+    M, N, K = 256 * 74 * 3 + 100, 512, 1024
+    a, b = i8((M, K), 13), i8((N, K), 14)
+    got = ops.gemm_i8(a.cuda(), b.cuda()).cpu().numpy()
+    rows = np.arange(0, M, 1009)
+    assert np.array_equal(got[rows], O.matmul_i8(a.numpy(), b.numpy(), rows=rows))
