@@ -406,6 +406,32 @@ void checkGraph(const TensorGraph& g) {
 // ============================================================ executor ====
 namespace {
 
+// int8 matmul plumbing: graph ints live in f32 storage; K1c wants int8
+// operands with 16-byte row pitches (B K-major) and returns int32 / int8.
+__global__ void ints_to_i8_kernel(const float* __restrict__ x, int8_t* __restrict__ y,
+                                  int64_t rows, int64_t cols, int64_t ldy, int transpose) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const int8_t v = static_cast<int8_t>(x[i]);  // an i8 tensor holds exact values in [-128, 127]
+    if (transpose) y[c * ldy + r] = v;  // x [rows = K, cols = N] -> y [N, K]
+    else y[r * ldy + c] = v;
+  }
+}
+
+__global__ void ints_to_f32_kernel(const void* __restrict__ x, float* __restrict__ y, int64_t n,
+                                   int bytes) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = bytes == 4 ? static_cast<float>(static_cast<const int32_t*>(x)[i])
+                      : static_cast<float>(static_cast<const int8_t*>(x)[i]);
+}
+
+unsigned elem_grid(int64_t n) {
+  return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+}
+
 // device storage type for a declared element type (ints carried exactly in f32)
 afg_dtype dev_type(ElementType t) {
   switch (t) {
@@ -808,6 +834,32 @@ class Executor {
       const int64_t cols = a.shape.back();
       ok(afg_softmax_lastdim(a.ptr, y.ptr, a.n / cols, cols, a.dt, y.dt, s_));
       plan("afg_softmax_lastdim -> " + n.output);
+    } else if (op == "matmul" && in(0).et == ElementType::I8 && in(1).et == ElementType::I8 &&
+               g_.find(n.output) && g_.find(n.output)->dtype == ElementType::I32) {
+      // i8 x i8 -> i32 (the quant path): exact integer
+      // accumulation on K1c (the interpreter's per-step I32 stores never
+      // saturate for K < 131072). An i8 OUTPUT is not routed here: the
+      // interpreter saturates every partial sum (e.g. 100+100-100 -> 27).
+      const DevBuf& a = in(0);
+      const DevBuf& b = in(1);
+      DevBuf& y = alloc(n.output);
+      const int64_t M = a.shape[0], K = a.shape[1], N = b.shape[1];
+      const int64_t Kp = (K + 15) / 16 * 16;
+      int8_t* a8 = static_cast<int8_t*>(scratch(static_cast<size_t>(M * Kp)));
+      int8_t* b8 = static_cast<int8_t*>(scratch(static_cast<size_t>(N * Kp)));
+      ints_to_i8_kernel<<<elem_grid(M * K), 256, 0, s_>>>(static_cast<const float*>(a.ptr), a8, M,
+                                                           K, Kp, 0);
+      ints_to_i8_kernel<<<elem_grid(K * N), 256, 0, s_>>>(static_cast<const float*>(b.ptr), b8, K,
+                                                           N, Kp, 1);
+      count_launch(2);
+      const bool i32 = true;
+      void* c = scratch(static_cast<size_t>(M * N * (i32 ? 4 : 1)));
+      ok(afg_gemm_i8(a8, Kp, b8, Kp, c, N, M, N, K, i32 ? 0 : 1, 1.0f, s_));
+      ints_to_f32_kernel<<<elem_grid(M * N), 256, 0, s_>>>(c, static_cast<float*>(y.ptr), M * N,
+                                                            i32 ? 4 : 1);
+      count_launch();
+      ok(cuda_status(cudaGetLastError(), "graph int8 matmul conversions"));
+      plan("afg_gemm_i8 -> " + n.output);
     } else if (op == "matmul") {
       const DevBuf& a = in(0);
       const DevBuf& b = in(1);

@@ -72,3 +72,15 @@ def test_missing_input_is_interp_error(cuda):
     case = GOLD[0]
     with pytest.raises(AfgError, match="missing input"):
         execute(case["graph"], {})
+
+
+def test_int8_matmul_graphs_run_on_k1c_bit_exact(cuda):
+    """i8 x i8 -> i32 matmul graphs (the quant path) execute on the int8 tensor
+    core kernel and reproduce the reference interpreter's outputs exactly
+    (tests/golden/int8_matmul.json, from oracle/_ref)."""
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "int8_matmul.json")))
+    for c in gold["cases"]:
+        out, plan = execute(c["graph"], {"a": np.array(c["a"]), "b": np.array(c["b"])},
+                            want_plan=True)
+        assert any("afg_gemm_i8" in p for p in plan), plan
+        assert np.array_equal(out["%c"], np.array(c["c"], dtype=np.float64)), c["name"]
