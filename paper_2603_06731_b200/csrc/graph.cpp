@@ -428,6 +428,25 @@ __global__ void ints_to_f32_kernel(const void* __restrict__ x, float* __restrict
                       : static_cast<float>(static_cast<const int8_t*>(x)[i]);
 }
 
+// Integer-typed matmul output other than the K1c case: the interpreter's
+// nest exactly — C = 0; for k: C = store_int(fma(a, b, C)) with the I8 / I32
+// store rounding nearbyint + saturate applied to every partial sum
+// (frontend.cpp:679-733, interp.cpp:88-104, :502-561), one thread per output.
+__global__ void int_matmul_sat_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                      float* __restrict__ c, int64_t M, int64_t N, int64_t K,
+                                      double lo, double hi) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < M * N;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / N, col = i % N;
+    double acc = 0.0;
+    for (int64_t k = 0; k < K; ++k) {
+      acc = fma(static_cast<double>(a[r * K + k]), static_cast<double>(b[k * N + col]), acc);
+      acc = fmin(fmax(nearbyint(acc), lo), hi);
+    }
+    c[i] = static_cast<float>(acc);
+  }
+}
+
 unsigned elem_grid(int64_t n) {
   return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
 }
@@ -860,6 +879,22 @@ class Executor {
       count_launch();
       ok(cuda_status(cudaGetLastError(), "graph int8 matmul conversions"));
       plan("afg_gemm_i8 -> " + n.output);
+    } else if (op == "matmul" && g_.find(n.output) &&
+               (g_.find(n.output)->dtype == ElementType::I8 ||
+                g_.find(n.output)->dtype == ElementType::I32) &&
+               in(0).dt == AFG_F32 && in(1).dt == AFG_F32) {
+      const DevBuf& a = in(0);
+      const DevBuf& b = in(1);
+      DevBuf& y = alloc(n.output);
+      const int64_t M = a.shape[0], K = a.shape[1], N = b.shape[1];
+      const bool i8 = y.et == ElementType::I8;
+      int_matmul_sat_kernel<<<elem_grid(M * N), 256, 0, s_>>>(
+          static_cast<const float*>(a.ptr), static_cast<const float*>(b.ptr),
+          static_cast<float*>(y.ptr), M, N, K, i8 ? -128.0 : -2147483648.0,
+          i8 ? 127.0 : 2147483647.0);
+      count_launch();
+      ok(cuda_status(cudaGetLastError(), "graph integer matmul"));
+      plan("int_matmul_sat -> " + n.output);
     } else if (op == "matmul") {
       const DevBuf& a = in(0);
       const DevBuf& b = in(1);

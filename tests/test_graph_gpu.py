@@ -84,3 +84,20 @@ def test_int8_matmul_graphs_run_on_k1c_bit_exact(cuda):
                             want_plan=True)
         assert any("afg_gemm_i8" in p for p in plan), plan
         assert np.array_equal(out["%c"], np.array(c["c"], dtype=np.float64)), c["name"]
+
+
+def test_int8_output_matmul_saturates_every_partial_sum(cuda):
+    """An i8-output matmul graph: the interpreter saturates each partial sum
+    (100 + 100 - 100 -> 127 - 100 = 27); the executor's integer nest does too."""
+    g = {"tensors": [{"id": "a", "shape": [2, 3], "dtype": "i8"},
+                     {"id": "b", "shape": [3, 2], "dtype": "i8"},
+                     {"id": "c", "shape": [2, 2], "dtype": "i8"}],
+         "ops": [{"op": "matmul", "inputs": ["a", "b"], "output": "c"}]}
+    a = np.array([[100, 100, -100], [-100, -100, 100]])
+    b = np.array([[1, 2], [1, 0], [1, -1]])
+    out, plan = execute(g, {"a": a, "b": b}, want_plan=True)
+    assert any("int_matmul_sat" in p for p in plan), plan
+    # reference: [[27, 127], [-28, -128]] (-100 - 100 -> -128, + 100 -> -28)
+    assert out["%c"].tolist() == [[27.0, 127.0], [-28.0, -128.0]]
+    if O.ref_available():
+        assert np.array_equal(out["%c"], O.ref_run(json.dumps(g), {"a": a, "b": b})["%c"])
