@@ -887,7 +887,13 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
                    cudaStream_t stream) {
   const bool b_mn_major = b_layout == AFG_B_KN;
   // BLOCK_N: 256 when N is large enough to fill it, else 128 / 64.
-  const int block_n = N >= 256 ? 256 : (N > 64 ? 128 : 64);
+  static const int bn_env = [] {  // A/B knob: AFG_GEMM_BN = 64 | 128 | 256 forces BLOCK_N
+    const char* e = getenv("AFG_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  const int block_n = (bn_env == 64 || bn_env == 128 || bn_env == 256)
+                          ? bn_env
+                          : (N >= 256 ? 256 : (N > 64 ? 128 : 64));
   // 256 x 256 tiles on a CTA pair when there are enough of them to fill the GPU
   const bool pair = use_pair_tiles(block_n, M, N, K);
   const CUtensorMapDataType tdt =
