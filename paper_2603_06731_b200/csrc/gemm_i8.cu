@@ -14,9 +14,10 @@
 // ring of half-B stages when the tiles fill the GPU), warp 2 owns 512 TMEM columns (two
 // 256-column s32 accumulators: the epilogue of tile i overlaps the MMAs of
 // tile i+1), warps 4-11 (two warpgroups, alternate 32-column chunks) read the
-// accumulator rows back (one row per thread) and store them. The scaling math runs in double, as the reference's
-// interpreter does (interp.cpp:502-561), so requantised / dequantised outputs
-// round exactly like the oracle.
+// accumulator rows back (one row per thread) and store them. Requantised /
+// dequantised outputs round exactly like the reference's double arithmetic
+// (interp.cpp:502-561): fp32 with an error-free product residual where that is
+// provably identical, double otherwise.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -57,6 +58,7 @@ struct I8Args {
   void* C;
   int mode;  // 0 i32, 1 requantised i8, 2 dequantised f32
   double scale;
+  float scale_f;  // the same value (the C ABI passes a float)
   int nmb, nnb;
 };
 
@@ -79,10 +81,37 @@ __device__ __forceinline__ void mma_i8_if(bool leader, uint32_t tmem_d, uint64_t
       : "memory");
 }
 
-// round half away from zero, saturate to [-128, 127] (interp quant)
+// round half away from zero, saturate to [-128, 127] (interp quant), in double
 __device__ __forceinline__ int requant_i8(int acc, double scale) {
   const double r = round(static_cast<double>(acc) * scale);
   return static_cast<int>(fmin(fmax(r, -128.0), 127.0));
+}
+
+// The same result in fp32, exactly: for |acc| < 2^24 the float acc is exact,
+// y = acc * s is the correctly rounded product and e = fma(acc, s, -y) its
+// exact residual (acc * s = y + e). Rounding y + e half away from zero only
+// needs e at an exact .5 fraction of y (elsewhere |f| <= 0.5 - ulp(y) and
+// |e| <= ulp(y) / 2 cannot cross the boundary). Larger |acc|: the double path.
+__device__ __forceinline__ int requant_i8_fast(int acc, float s, double sd) {
+  if (acc > -(1 << 24) && acc < (1 << 24)) {
+    const float a = static_cast<float>(acc);
+    const float y = a * s;
+    const float e = fmaf(a, s, -y);
+    const float r = truncf(y);
+    const float f = fabsf(y - r);
+    const bool away = f > 0.5f || (f == 0.5f && (e == 0.0f || (e > 0.0f) == (y > 0.0f)));
+    const float q = away ? r + copysignf(1.0f, y) : r;
+    return static_cast<int>(fminf(fmaxf(q, -128.0f), 127.0f));
+  }
+  return requant_i8(acc, sd);
+}
+
+// (float)(acc * scale) as the reference computes it (double product, one
+// rounding to f32): for |acc| < 2^24 the double product is exact, so the fp32
+// product (one correct rounding) is the same value.
+__device__ __forceinline__ float dequant_f32(int acc, float s, double sd) {
+  if (acc > -(1 << 24) && acc < (1 << 24)) return static_cast<float>(acc) * s;
+  return static_cast<float>(static_cast<double>(acc) * sd);
 }
 
 __device__ __forceinline__ void store_row32(const uint32_t (&r)[32], const I8Args& a, int row,
@@ -108,7 +137,9 @@ __device__ __forceinline__ void store_row32(const uint32_t (&r)[32], const I8Arg
       uint32_t x = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b)
-        x |= (static_cast<uint32_t>(requant_i8(static_cast<int>(r[4 * v + b]), a.scale)) & 0xffu)
+        x |= (static_cast<uint32_t>(requant_i8_fast(static_cast<int>(r[4 * v + b]), a.scale_f,
+                                                     a.scale)) &
+              0xffu)
              << (8 * b);
       w[v] = x;
     }
@@ -125,7 +156,7 @@ __device__ __forceinline__ void store_row32(const uint32_t (&r)[32], const I8Arg
     float f[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      f[j] = static_cast<float>(static_cast<double>(static_cast<int>(r[j])) * a.scale);
+      f[j] = dequant_f32(static_cast<int>(r[j]), a.scale_f, a.scale);
     if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
       for (int v = 0; v < 8; ++v)
@@ -362,6 +393,7 @@ afg_status gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void*
   a.C = C;
   a.mode = mode;
   a.scale = scale;
+  a.scale_f = static_cast<float>(scale);
   a.nmb = static_cast<int>((M + (pair ? 2 : 1) * I8_BM - 1) / ((pair ? 2 : 1) * I8_BM));
   a.nnb = static_cast<int>((N + I8_BN - 1) / I8_BN);
   const cudaError_t e = pair ? launch_i8<true>(tmA, tmB, a, stream) : launch_i8<false>(tmA, tmB, a, stream);

@@ -48,7 +48,8 @@ def test_i32_exact(cuda, M, N, K):
     assert np.array_equal(got if rows is None else got[rows], want)
 
 
-@pytest.mark.parametrize("mode,scale", [(1, 1 / 4096), (1, 0.5), (2, 3.1e-5)])
+@pytest.mark.parametrize("mode,scale", [(1, 1 / 4096), (1, 0.5), (2, 3.1e-5), (1, 1 / 1000.3),
+                                        (1, 0.013), (2, 0.1)])
 def test_requant_and_dequant(cuda, mode, scale):
     M, N, K = 300, 384, 512
     a, b = i8((M, K), 5), i8((N, K), 6)
@@ -93,3 +94,17 @@ def test_pair_tiles_long_k_many_per_cluster(cuda):
     got = ops.gemm_i8(a.cuda(), b.cuda()).cpu().numpy()
     rows = np.arange(0, M, 1009)
     assert np.array_equal(got[rows], O.matmul_i8(a.numpy(), b.numpy(), rows=rows))
+
+
+@pytest.mark.parametrize("mode,scale", [(1, 1 / 140000.7), (2, 1e-3)])
+def test_large_accumulators_take_the_double_path(cuda, mode, scale):
+    """|acc| >= 2^24 (float no longer exact): the epilogue's double fallback."""
+    M, N, K = 128, 256, 1088
+    a = torch.full((M, K), 127, dtype=torch.int8)
+    a[1::2] = -127
+    b = torch.full((N, K), 127, dtype=torch.int8)
+    b[:, ::3] = 126
+    got = ops.gemm_i8(a.cuda(), b.cuda(), out_mode=mode, scale=scale).cpu().numpy()
+    want = O.matmul_i8(a.numpy(), b.numpy(), mode=mode, scale=scale)
+    assert np.abs(O.matmul_i8(a.numpy(), b.numpy())).min() >= 2**24
+    assert np.array_equal(got, want)
