@@ -228,6 +228,17 @@ AFG_API afg_status afg_gemm_i8(const void* A, int64_t lda, const void* B, int64_
                                int64_t ldc, int64_t M, int64_t N, int64_t K, int out_mode,
                                float scale, void* stream);
 
+/* int8 implicit-GEMM convolution (the conv half of the quant path; K1c on
+ * TMA im2col): x i8 NHWC [B,H,W,C], w i8 OHWI [OC,KH,KW,C], output NHWC
+ * [B*OH*OW, OC] as afg_gemm_i8's out_mode / scale (i32 exact, requantised i8,
+ * dequantised f32). C % 16 == 0; explicit pad_top / pad_left (the far-side
+ * padding follows from OH / OW), stride / dilation as afg_conv2d_nhwc. */
+AFG_API afg_status afg_conv2d_nhwc_i8(const void* x, const void* w, void* y, int64_t B, int64_t H,
+                                      int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
+                                      int64_t stride_h, int64_t stride_w, int64_t pad_top,
+                                      int64_t pad_left, int64_t dil_h, int64_t dil_w, int64_t OH,
+                                      int64_t OW, int out_mode, float scale, void* stream);
+
 /* Quantisation chain (interp.cpp quant/dequant; oracles.cpp:387-398):
  *  mode 0 quantize  : y = clamp(round_half_away(x / scale), -128, 127)
  *  mode 1 dequantize: y = x * scale

@@ -197,6 +197,38 @@ def matmul_i8(A, B_nk, mode=0, scale=1.0, rows=None):
     return x.astype(np.float32)
 
 
+def conv_i8(x, w_ohwi, stride=(1, 1), pad=(0, 0), dil=(1, 1), out_hw=None, mode=0, scale=1.0):
+    """Exact integer NHWC conv (the reference's i8 conv graph nest,
+    frontend.cpp:752-970, evaluated in double = exact integers), i32 result,
+    then matmul_i8's requantise / dequantise. x [B,H,W,C], w [OC,KH,KW,C]."""
+    x = np.asarray(x, dtype=np.int64)
+    w = np.asarray(w_ohwi, dtype=np.int64)
+    B, H, W, C = x.shape
+    OC, KH, KW, _ = w.shape
+    if out_hw is None:
+        out_hw = ((H + 2 * pad[0] - dil[0] * (KH - 1) - 1) // stride[0] + 1,
+                  (W + 2 * pad[1] - dil[1] * (KW - 1) - 1) // stride[1] + 1)
+    OH, OW = out_hw
+    hp = max(H + pad[0], (OH - 1) * stride[0] + (KH - 1) * dil[0] + 1)
+    wp = max(W + pad[1], (OW - 1) * stride[1] + (KW - 1) * dil[1] + 1)
+    xp = np.zeros((B, hp, wp, C), dtype=np.int64)
+    xp[:, pad[0]:pad[0] + H, pad[1]:pad[1] + W, :] = x
+    acc = np.zeros((B, OH, OW, OC), dtype=np.int64)
+    for ky in range(KH):
+        for kx in range(KW):
+            ys, xs = ky * dil[0], kx * dil[1]
+            patch = xp[:, ys:ys + (OH - 1) * stride[0] + 1:stride[0],
+                       xs:xs + (OW - 1) * stride[1] + 1:stride[1], :]
+            acc += np.einsum("bhwc,oc->bhwo", patch, w[:, ky, kx, :])
+    acc = np.clip(acc, -2**31, 2**31 - 1)
+    if mode == 0:
+        return acc.astype(np.int32)
+    v = acc.astype(np.float64) * np.float64(np.float32(scale))
+    if mode == 1:
+        return np.clip(np.sign(v) * np.floor(np.abs(v) + 0.5), -128, 127).astype(np.int8)
+    return v.astype(np.float32)
+
+
 # ----------------------------------------------------------------- conv ---
 
 def conv_geometry(inH, inW, kH, kW, stride=(1, 1), dil=(1, 1), same=False, transposed=False):

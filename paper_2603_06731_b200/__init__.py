@@ -103,6 +103,7 @@ _SIGS = {
     "afg_broadcast_in_dim": (_i, [_P, _P, _i, _P, _i, _P, _P, _i, _i, _P]),
     "afg_quantize": (_i, [_P, _P, _I, _f, _i, _i, _i, _P]),
     "afg_gemm_i8": (_i, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _i, _f, _P]),
+    "afg_conv2d_nhwc_i8": (_i, [_P, _P, _P] + [_I] * 15 + [_i, _f, _P]),
     "afg_graph_run": (_i, [ctypes.c_char_p, _i, ctypes.POINTER(ctypes.c_char_p),
                            ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
                            ctypes.POINTER(_I), _i, _P, ctypes.POINTER(_P)]),

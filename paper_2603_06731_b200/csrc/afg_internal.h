@@ -37,7 +37,8 @@ afg_status make_tmap(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
 // lower/upper = {W, H} bounding-box corners, traversal strides sw/sh.
 afg_status make_tmap_im2col_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
                                int64_t C, int64_t W, int64_t H, int64_t N, const int* lower,
-                               const int* upper, int sw, int sh, int channels, int pixels);
+                               const int* upper, int sw, int sh, int channels, int pixels,
+                               int elem_bytes = 2);
 
 inline int dtype_bytes(afg_dtype t) { return t == AFG_F32 ? 4 : 2; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -135,12 +135,13 @@ afg_status make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType 
 
 afg_status make_tmap_im2col_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
                                int64_t C, int64_t W, int64_t H, int64_t N, const int* lower,
-                               const int* upper, int sw, int sh, int channels, int pixels) {
+                               const int* upper, int sw, int sh, int channels, int pixels,
+                               int elem_bytes) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return set_error(AFG_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable (driver)");
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W),
                               static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(N)};
-  const cuuint64_t es = 2;
+  const cuuint64_t es = static_cast<cuuint64_t>(elem_bytes);
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * es,
                                  static_cast<cuuint64_t>(C * W) * es,
                                  static_cast<cuuint64_t>(C * W * H) * es};

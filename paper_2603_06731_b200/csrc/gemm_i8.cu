@@ -60,6 +60,8 @@ struct I8Args {
   double scale;
   float scale_f;  // the same value (the C ABI passes a float)
   int nmb, nnb;
+  // implicit-GEMM conv (IM2COL): K slab kb = (filter tap, 128-channel block)
+  int c_blocks, taps, KW, dil_w, dil_h, OH, OW, stride_w, stride_h, lower_w, lower_h;
 };
 
 // tcgen05 instruction descriptor, kind::i8: D = s32, A = B = signed 8-bit,
@@ -169,10 +171,11 @@ __device__ __forceinline__ void store_row32(const uint32_t (&r)[32], const I8Arg
   }
 }
 
-template <bool PAIR>
+template <bool PAIR, bool IM2COL = false>
 __global__ void __launch_bounds__(384, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const I8Args args) {
+  static_assert(!(PAIR && IM2COL), "the int8 conv runs single-CTA tiles");
   using L = I8Smem<PAIR>;
   constexpr int NS = L::STAGES;
   constexpr int TILE_M = PAIR ? 2 * I8_BM : I8_BM;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(384, 1)
   griddep_launch_dependents();
 
   const int num_tiles = args.nmb * args.nnb;
-  const int num_kb = (args.K + I8_BK - 1) / I8_BK;
+  const int num_kb = IM2COL ? args.taps * args.c_blocks : (args.K + I8_BK - 1) / I8_BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -232,7 +235,23 @@ __global__ void __launch_bounds__(384, 1)
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           // PAIR: both CTAs' bytes complete on the leader's full barrier
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], (PAIR ? 2 : 1) * L::STAGE_BYTES);
-          if constexpr (PAIR) {
+          if constexpr (IM2COL) {
+            // 128 output pixels x 128 channels of one filter tap, gathered by
+            // the TMA unit in im2col mode (zero fill = padding / channel tail);
+            // B = the OHWI filter as [OC, taps, C] (channel tail zero-filled)
+            const int q = m0 % args.OW;
+            const int p = (m0 / args.OW) % args.OH;
+            const int n = m0 / (args.OW * args.OH);
+            const int tap = kb / args.c_blocks;
+            const int cb = kb - tap * args.c_blocks;
+            const int ky = tap / args.KW;
+            const int kx = tap - ky * args.KW;
+            tma_load_im2col_4d(sa, &tmA, &full_bar[stage], cb * I8_BK,
+                               args.lower_w + q * args.stride_w, args.lower_h + p * args.stride_h,
+                               n, static_cast<uint16_t>(kx * args.dil_w),
+                               static_cast<uint16_t>(ky * args.dil_h));
+            tma_load_3d(sa + L::A_BYTES, &tmB, &full_bar[stage], cb * I8_BK, tap, n0);
+          } else if constexpr (PAIR) {
             const uint32_t fb = mapa_shared(&full_bar[stage], 0);
             tma_load_2d_pair(sa, &tmA, fb, kb * I8_BK, m0);
             tma_load_2d_pair(sa + L::A_BYTES, &tmB, fb, kb * I8_BK, n0);
@@ -328,13 +347,13 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <bool PAIR>
+template <bool PAIR, bool IM2COL = false>
 cudaError_t launch_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const I8Args& a,
                       cudaStream_t stream) {
   constexpr int smem = I8Smem<PAIR>::TOTAL;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<PAIR>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<PAIR, IM2COL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -362,7 +381,7 @@ cudaError_t launch_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const I8Ar
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<PAIR>, tmA, tmB, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<PAIR, IM2COL>, tmA, tmB, a);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -400,6 +419,58 @@ afg_status gemm_i8(const void* A, int64_t lda, const void* B, int64_t ldb, void*
   return cuda_status(e, "gemm_i8 launch");
 }
 
+// int8 implicit-GEMM convolution (NHWC activations, OHWI filter), the conv
+// half of the quant path: M = B*OH*OW output pixels, N = OC, K = taps x C.
+afg_status conv_i8(const void* x, const void* w, void* y, int64_t B, int64_t H, int64_t W,
+                   int64_t C, int64_t OC, int64_t KH, int64_t KW, int64_t sh, int64_t sw,
+                   int64_t pt, int64_t pl, int64_t dh, int64_t dw, int64_t OH, int64_t OW,
+                   int mode, double scale, cudaStream_t stream) {
+  const int64_t pb = (OH - 1) * sh + (KH - 1) * dh + 1 - H - pt;
+  const int64_t pr = (OW - 1) * sw + (KW - 1) * dw + 1 - W - pl;
+  const int lower[2] = {static_cast<int>(-pl), static_cast<int>(-pt)};
+  const int upper[2] = {static_cast<int>(pr - (KW - 1) * dw), static_cast<int>(pb - (KH - 1) * dh)};
+  for (int i = 0; i < 2; ++i)
+    if (lower[i] < -128 || lower[i] > 127 || upper[i] < -128 || upper[i] > 127)
+      return set_error(AFG_ERR_UNSUPPORTED, "conv_i8: padding outside the im2col corner range");
+  if (sh > 8 || sw > 8) return set_error(AFG_ERR_UNSUPPORTED, "conv_i8: stride > 8");
+  CUtensorMap tmA, tmB;
+  afg_status st = make_tmap_im2col_4d(&tmA, x, CU_TENSOR_MAP_DATA_TYPE_UINT8, C, W, H, B, lower,
+                                      upper, static_cast<int>(sw), static_cast<int>(sh), I8_BK,
+                                      I8_BM, 1);
+  if (st != AFG_OK) return st;
+  const uint64_t dims[3] = {static_cast<uint64_t>(C), static_cast<uint64_t>(KH * KW),
+                            static_cast<uint64_t>(OC)};
+  const uint64_t strides[2] = {static_cast<uint64_t>(C), static_cast<uint64_t>(KH * KW * C)};
+  const uint32_t box[3] = {static_cast<uint32_t>(I8_BK), 1u, static_cast<uint32_t>(I8_BN)};
+  st = make_tmap(&tmB, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, dims, strides, box,
+                 CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != AFG_OK) return st;
+  I8Args a{};
+  const int64_t M = B * OH * OW;
+  a.M = static_cast<int>(M);
+  a.N = static_cast<int>(OC);
+  a.K = static_cast<int>(KH * KW * C);
+  a.ldc = OC;
+  a.C = y;
+  a.mode = mode;
+  a.scale = scale;
+  a.scale_f = static_cast<float>(scale);
+  a.nmb = static_cast<int>((M + I8_BM - 1) / I8_BM);
+  a.nnb = static_cast<int>((OC + I8_BN - 1) / I8_BN);
+  a.c_blocks = static_cast<int>((C + I8_BK - 1) / I8_BK);
+  a.taps = static_cast<int>(KH * KW);
+  a.KW = static_cast<int>(KW);
+  a.dil_w = static_cast<int>(dw);
+  a.dil_h = static_cast<int>(dh);
+  a.OH = static_cast<int>(OH);
+  a.OW = static_cast<int>(OW);
+  a.stride_w = static_cast<int>(sw);
+  a.stride_h = static_cast<int>(sh);
+  a.lower_w = lower[0];
+  a.lower_h = lower[1];
+  return cuda_status(launch_i8<false, true>(tmA, tmB, a, stream), "conv_i8 launch");
+}
+
 }  // namespace afg
 
 using namespace afg;
@@ -422,5 +493,31 @@ extern "C" afg_status afg_gemm_i8(const void* A, int64_t lda, const void* B, int
   afg_status st = check_device();
   if (st != AFG_OK) return st;
   return gemm_i8(A, lda, B, ldb, C, ldc, M, N, K, out_mode, static_cast<double>(scale),
+                 static_cast<cudaStream_t>(stream));
+}
+
+extern "C" afg_status afg_conv2d_nhwc_i8(const void* x, const void* w, void* y, int64_t B, int64_t H,
+                                         int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
+                                         int64_t stride_h, int64_t stride_w, int64_t pad_top,
+                                         int64_t pad_left, int64_t dil_h, int64_t dil_w, int64_t OH,
+                                         int64_t OW, int out_mode, float scale, void* stream) {
+  if (!x || !w || !y) return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc_i8: null operand");
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || OC <= 0 || KH <= 0 || KW <= 0 || OH <= 0 ||
+      OW <= 0 || stride_h <= 0 || stride_w <= 0 || dil_h <= 0 || dil_w <= 0 || pad_top < 0 ||
+      pad_left < 0)
+    return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc_i8: bad geometry");
+  if (out_mode < 0 || out_mode > 2)
+    return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc_i8: bad out_mode %d", out_mode);
+  if (out_mode != 0 && !(scale > 0.0f))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc_i8: scale must be positive");
+  if (KH * KW * C >= (1ll << 17) || B * OH * OW >= (1ll << 31))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc_i8: extent out of range");
+  if (C % 16 != 0 || !aligned16(x) || !aligned16(w))
+    return set_error(AFG_ERR_UNSUPPORTED,
+                     "afg_conv2d_nhwc_i8: C must be a multiple of 16 with 16-byte aligned bases");
+  afg_status st = check_device();
+  if (st != AFG_OK) return st;
+  return conv_i8(x, w, y, B, H, W, C, OC, KH, KW, stride_h, stride_w, pad_top, pad_left, dil_h,
+                 dil_w, OH, OW, out_mode, static_cast<double>(scale),
                  static_cast<cudaStream_t>(stream));
 }

@@ -70,6 +70,26 @@ def gemm_i8(a, b_nk, out_mode=0, scale=1.0, out=None):
     return out
 
 
+def conv2d_nhwc_i8(x, w_ohwi, stride=(1, 1), pad=(0, 0), dil=(1, 1), out_hw=None, out_mode=0,
+                   scale=1.0):
+    """int8 implicit-GEMM conv (K1c on TMA im2col). x int8 [B,H,W,C], w int8
+    [OC,KH,KW,C]; pad = (top, left); out_hw defaults to symmetric padding.
+    Returns [B,OH,OW,OC] int32 / int8 / float32 by out_mode (as gemm_i8)."""
+    _need_cuda(x, w_ohwi)
+    B, H, W, C = x.shape
+    OC, KH, KW, _ = w_ohwi.shape
+    if out_hw is None:
+        out_hw = ((H + 2 * pad[0] - dil[0] * (KH - 1) - 1) // stride[0] + 1,
+                  (W + 2 * pad[1] - dil[1] * (KW - 1) - 1) // stride[1] + 1)
+    OH, OW = out_hw
+    od = {0: torch.int32, 1: torch.int8, 2: torch.float32}[int(out_mode)]
+    y = torch.empty((B, OH, OW, OC), dtype=od, device=x.device)
+    check(lib().afg_conv2d_nhwc_i8(_ptr(x.contiguous()), _ptr(w_ohwi.contiguous()), _ptr(y), B, H,
+                                   W, C, OC, KH, KW, stride[0], stride[1], pad[0], pad[1], dil[0],
+                                   dil[1], OH, OW, int(out_mode), float(scale), _stream()))
+    return y
+
+
 def gemm_batched(a, b, out_dtype=None):
     _need_cuda(a, b)
     *bd, M, K = a.shape

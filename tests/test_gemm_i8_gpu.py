@@ -108,3 +108,37 @@ def test_large_accumulators_take_the_double_path(cuda, mode, scale):
     want = O.matmul_i8(a.numpy(), b.numpy(), mode=mode, scale=scale)
     assert np.abs(O.matmul_i8(a.numpy(), b.numpy())).min() >= 2**24
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------------ int8 implicit-GEMM conv ---
+
+def test_conv_reference_fixtures_bit_exact(cuda):
+    for c in json.load(open(os.path.join(GOLD, "int8_matmul.json")))["conv_cases"]:
+        x = torch.from_numpy(np.ascontiguousarray(np.transpose(np.array(c["x"], dtype=np.int8),
+                                                               (0, 2, 3, 1))))
+        w = torch.from_numpy(np.ascontiguousarray(np.transpose(np.array(c["w"], dtype=np.int8),
+                                                               (0, 2, 3, 1))))
+        K = w.shape[1]
+        y = np.array(c["y"])
+        pad = (K // 2, K // 2) if c["padding"] == "same" else (0, 0)
+        got = ops.conv2d_nhwc_i8(x.cuda(), w.cuda(), stride=(c["stride"],) * 2, pad=pad,
+                                 out_hw=(y.shape[2], y.shape[3])).cpu().numpy()
+        assert np.array_equal(np.transpose(got, (0, 3, 1, 2)), y), c["name"]
+
+
+@pytest.mark.parametrize("B,H,C,OC,K,s,p", [(4, 28, 128, 128, 3, 1, 1), (2, 56, 64, 96, 3, 2, 1),
+                                            (4, 14, 256, 64, 1, 1, 0), (3, 13, 48, 40, 3, 1, 1),
+                                            (2, 7, 512, 300, 3, 1, 1)])
+def test_conv_shapes_i32_exact(cuda, B, H, C, OC, K, s, p):
+    x, w = i8((B, H, H, C), H + C), i8((OC, K, K, C), OC + K)
+    got = ops.conv2d_nhwc_i8(x.cuda(), w.cuda(), stride=(s, s), pad=(p, p)).cpu().numpy()
+    want = O.conv_i8(x.numpy(), w.numpy(), stride=(s, s), pad=(p, p))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("mode,scale", [(1, 1 / 3000.7), (2, 1e-3)])
+def test_conv_requant_and_dequant(cuda, mode, scale):
+    x, w = i8((2, 20, 20, 64), 31), i8((128, 3, 3, 64), 32)
+    got = ops.conv2d_nhwc_i8(x.cuda(), w.cuda(), pad=(1, 1), out_mode=mode, scale=scale)
+    want = O.conv_i8(x.numpy(), w.numpy(), pad=(1, 1), mode=mode, scale=scale)
+    assert np.array_equal(got.cpu().numpy(), want)

@@ -242,3 +242,18 @@ def test_int8_matmul_restatement_vs_live_reference():
          "ops": [{"op": "matmul", "inputs": ["a", "b"], "output": "c"}]}
     out = O.ref_run(json.dumps(g), {"a": a, "b": b}, "interpret")["%c"]
     assert np.array_equal(O.matmul_i8(a, b.T), out)
+
+
+def _pad_of(c, K):
+    return (K // 2, K // 2) if c["padding"] == "same" else (0, 0)
+
+
+def test_int8_conv_restatement_vs_reference_fixtures():
+    for c in json.load(open(os.path.join(GOLD, "int8_matmul.json")))["conv_cases"]:
+        x = np.transpose(np.array(c["x"]), (0, 2, 3, 1))
+        w = np.transpose(np.array(c["w"]), (0, 2, 3, 1))
+        K = w.shape[1]
+        y = np.array(c["y"])
+        got = O.conv_i8(x, w, stride=(c["stride"],) * 2, pad=_pad_of(c, K),
+                        out_hw=(y.shape[2], y.shape[3]))
+        assert np.array_equal(np.transpose(got, (0, 3, 1, 2)), y), c["name"]
