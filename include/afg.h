@@ -26,6 +26,8 @@
  *   afg_reduce_lastdim    <- lowerReduceShaped      frontend.cpp:628-675
  *   afg_gemm_i8           <- quant repositioning    SPEC.md:531-572 (quant.cpp
  *                            is a stub): i8 x i8 -> i32 matmul + requant
+ *   afg_conv2d_nhwc_i8    <- quant repositioning of lowerConv (frontend.cpp:
+ *                            752-970) as an i8 implicit GEMM + requant
  *
  * Conventions
  *  - All tensor pointers are caller-owned DEVICE pointers, dense row-major
