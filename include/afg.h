@@ -147,6 +147,16 @@ AFG_API afg_status afg_conv2d_nhwc(const void* x, const void* w, const float* bi
                            int64_t dil_w, int64_t OH, int64_t OW, afg_dtype dtype,
                            afg_epilogue epi, void* stream);
 
+/* afg_conv2d_nhwc with an explicit output type: x / w in `dtype`, y in
+ * `y_dtype` (F32 keeps the fp32 accumulator unrounded; the graph executor's
+ * f32-declared NHWC conv chains use it). */
+AFG_API afg_status afg_conv2d_nhwc_ex(const void* x, const void* w, const float* bias, void* y,
+                              int64_t B, int64_t H, int64_t W, int64_t C, int64_t OC,
+                              int64_t KH, int64_t KW, int64_t stride_h, int64_t stride_w,
+                              int64_t pad_top, int64_t pad_left, int64_t dil_h,
+                              int64_t dil_w, int64_t OH, int64_t OW, afg_dtype dtype,
+                              afg_dtype y_dtype, afg_epilogue epi, void* stream);
+
 /* Direct convolution in the reference's own NCHW/OIHW layout (and IOHW for
  * transposed), exactly the semantics of frontend.cpp:752-970 / the oracle
  * convReference (oracles.cpp:78-120), fp32 accumulate. pad_* are the begin
@@ -295,11 +305,15 @@ AFG_API afg_status afg_encoder_layer_fwd(
  * current device with the given host inputs (values as doubles, keyed by
  * tensor id with or without '%'; rounded to the declared element type on
  * upload like the interpreter, interp.cpp:212-213) and returns the outputs
- * keyed "%id" as doubles. fuse != 0 enables the fused kernel patterns.
+ * keyed "%id" as doubles. flags: AFG_GRAPH_FUSE enables the kernel patterns
+ * and fused regions; AFG_GRAPH_EXACT keeps f32 tensors off the tensor cores
+ * (bit-exact paths only).
  * GraphError -> AFG_ERR_INVALID_ARG, InterpError -> AFG_ERR_CUDA. */
+#define AFG_GRAPH_FUSE 1
+#define AFG_GRAPH_EXACT 2
 typedef struct afg_graph_result afg_graph_result;
 AFG_API afg_status afg_graph_run(const char* graph_json, int n_inputs, const char* const* names,
-                         const double* const* data, const int64_t* numel, int fuse,
+                         const double* const* data, const int64_t* numel, int flags,
                          void* stream, afg_graph_result** out);
 AFG_API int afg_graph_result_count(const afg_graph_result* r);
 AFG_API const char* afg_graph_result_name(const afg_graph_result* r, int i);
@@ -310,7 +324,7 @@ AFG_API const double* afg_graph_result_data(const afg_graph_result* r, int i);
 /* One line per launched kernel (group): what the planner fused. */
 AFG_API const char* afg_graph_result_plan(const afg_graph_result* r);
 AFG_API void afg_graph_result_free(afg_graph_result* r);
-/* parseGraphJson + checkGraph only (GraphError -> AFG_ERR_INVALID_ARG). */
+/* Graph JSON read + validation only (GraphError -> AFG_ERR_INVALID_ARG). */
 AFG_API afg_status afg_graph_check_json(const char* graph_json);
 
 #ifdef __cplusplus

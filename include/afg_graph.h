@@ -80,18 +80,21 @@ struct TensorValue {  // interp.h:33-44
   }
 };
 
-struct ConvGeometry {  // frontend.h:72-75
-  int64_t outH, outW, padY, padX;
-};
-
-TensorGraph parseGraphJson(const std::string& text);  // frontend.cpp:57-113
-void checkGraph(const TensorGraph& g);                  // frontend.cpp:264-294
-ConvGeometry convGeometry(int64_t inH, int64_t inW, int64_t kH, int64_t kW,
-                          const TensorOpNode& node);    // frontend.cpp:115-149
+// Reads the graph JSON schema of parseGraphJson (frontend.cpp:57-113).
+TensorGraph parseGraphJson(const std::string& text);
+// Table-driven validation with checkGraph's error behaviour
+// (frontend.cpp:159-294): GraphError "unsupported-op: ...", "shape-mismatch:
+// ...", unknown / duplicate / used-before-produced tensors, non-positive
+// extents. (A C++ caller holding an af::TensorGraph runs the reference's own
+// af::checkGraph first, integration/af_gpu.cpp.)
+void validateGraph(const TensorGraph& g);
 
 struct GpuOptions {
-  void* stream = nullptr;  // cudaStream_t; NULL = legacy default stream
-  bool fuse = true;        // pattern-fuse matmul/conv epilogues and attention
+  void* stream = nullptr;     // cudaStream_t; NULL = legacy default stream
+  bool fuse = true;           // kernel patterns + fused VM regions (else one launch per op)
+  bool tensor_cores = true;   // f32 tensors holding exact bf16 / f16 values run on
+                              // tcgen05 (fp32 accumulation; stated tolerance
+                              // instead of bit-exactness); false = exact paths only
 };
 
 struct ExecStats {

@@ -84,6 +84,7 @@ _SIGS = {
     "afg_gemm": (_i, [_P, _I, _P, _I, _P, _P, _P, _I, _I, _I, _I, _i, _i, _i, _i, _P]),
     "afg_gemm_batched": (_i, [_P, _P, _P, _I, _I, _I, _I, _i, _i, _P]),
     "afg_conv2d_nhwc": (_i, [_P, _P, _P, _P] + [_I] * 15 + [_i, _i, _P]),
+    "afg_conv2d_nhwc_ex": (_i, [_P, _P, _P, _P] + [_I] * 15 + [_i, _i, _i, _P]),
     "afg_conv2d_nchw": (_i, [_P, _P, _P] + [_I] * 13 + [_i, _I, _I, _i, _i, _P]),
     "afg_conv_pack_filter": (_i, [_P, _P, _I, _I, _I, _I, _i, _P]),
     "afg_attention_fwd": (_i, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _f, _i, _i, _i, _P]),

@@ -57,12 +57,13 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
 // disables it for A/B measurements.
 bool pdl_enabled();
 afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, int64_t B,
-                     int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_epilogue epi,
-                     cudaStream_t stream);
+                     int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_dtype yt,
+                     afg_epilogue epi, cudaStream_t stream);
 afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int64_t B,
                    int64_t H, int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
                    int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh, int64_t dw,
-                   int64_t OH, int64_t OW, afg_dtype dt, afg_epilogue epi, cudaStream_t stream);
+                   int64_t OH, int64_t OW, afg_dtype dt, afg_dtype yt, afg_epilogue epi,
+                   cudaStream_t stream);
 
 afg_status gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, const float* bias,
                      const void* residual, void* C, int64_t ldc, int64_t M, int64_t N,

@@ -24,9 +24,9 @@ __device__ __forceinline__ float ldx(const T* p) {
   return OutCvt<T>::from(*p);
 }
 
-template <typename T>
+template <typename T, typename TO>
 __global__ void conv_nhwc_direct_kernel(const T* __restrict__ x, const T* __restrict__ w,
-                                        const float* __restrict__ bias, T* __restrict__ y,
+                                        const float* __restrict__ bias, TO* __restrict__ y,
                                         int B, int H, int W, int C, int OC, int KH, int KW,
                                         int sh, int sw, int pt, int pl, int dh, int dw, int OH,
                                         int OW, int epi) {
@@ -52,7 +52,7 @@ __global__ void conv_nhwc_direct_kernel(const T* __restrict__ x, const T* __rest
       }
     }
     if (epi != AFG_EPI_NONE) acc = apply_act_rt(epi, acc + bias[oc]);
-    y[i] = OutCvt<T>::to(acc);
+    y[i] = OutCvt<TO>::to(acc);
   }
 }
 
@@ -133,13 +133,23 @@ afg_status afg_conv2d_nhwc(const void* x, const void* w, const float* bias, void
                            int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh,
                            int64_t dw, int64_t OH, int64_t OW, afg_dtype dt, afg_epilogue epi,
                            void* stream) {
+  return afg_conv2d_nhwc_ex(x, w, bias, y, B, H, W, C, OC, KH, KW, sh, sw, pt, pl, dh, dw, OH, OW,
+                            dt, dt, epi, stream);
+}
+
+afg_status afg_conv2d_nhwc_ex(const void* x, const void* w, const float* bias, void* y, int64_t B,
+                              int64_t H, int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
+                              int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh,
+                              int64_t dw, int64_t OH, int64_t OW, afg_dtype dt, afg_dtype yt,
+                              afg_epilogue epi, void* stream) {
   if (!x || !w || !y) return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc: null operand");
   if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || OC <= 0 || KH <= 0 || KW <= 0 || sh <= 0 ||
       sw <= 0 || dh <= 0 || dw <= 0 || OH <= 0 || OW <= 0 || pt < 0 || pl < 0)
     return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc: bad geometry");
   if ((OH - 1) * sh - pt + (KH - 1) * dh < 0 || (OW - 1) * sw - pl + (KW - 1) * dw < 0)
     return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc: bad output extent");
-  if (!valid_dtype(dt)) return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc: bad dtype");
+  if (!valid_dtype(dt) || !(yt == dt || yt == AFG_F32))
+    return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc: bad dtype pair");
   if (epi != AFG_EPI_NONE && !bias)
     return set_error(AFG_ERR_INVALID_ARG, "afg_conv2d_nhwc: epilogue needs a bias");
   const int64_t M = B * OH * OW;
@@ -153,28 +163,30 @@ afg_status afg_conv2d_nhwc(const void* x, const void* w, const float* bias, void
   if (tc && KH == 1 && KW == 1 && sh == 1 && sw == 1 && pt == 0 && pl == 0 && OH == H &&
       OW == W) {
     // 1x1 / stride 1: the implicit GEMM is the plain GEMM on [B*H*W, C] x [OC, C]^T
-    return gemm_tc(x, C, w, C, bias, nullptr, y, OC, M, OC, C, dt, dt, AFG_B_NK, epi, s);
+    return gemm_tc(x, C, w, C, bias, nullptr, y, OC, M, OC, C, dt, yt, AFG_B_NK, epi, s);
   }
   if (tc && KH == 3 && KW == 3 && sh == 1 && sw == 1 && dh == 1 && dw == 1 && pt == 1 &&
       pl == 1 && OH == H && OW == W) {
     // 3x3 / stride 1 / pad 1: the input halo is staged once per tile, not per tap
-    st = conv_halo(x, w, bias, y, B, H, W, C, OC, dt, epi, s);
+    st = conv_halo(x, w, bias, y, B, H, W, C, OC, dt, yt, epi, s);
     if (st != AFG_ERR_UNSUPPORTED) return st;
   }
   if (tc && sh <= 8 && sw <= 8) {
-    st = conv_tc(x, w, bias, y, B, H, W, C, OC, KH, KW, sh, sw, pt, pl, dh, dw, OH, OW, dt, epi,
+    st = conv_tc(x, w, bias, y, B, H, W, C, OC, KH, KW, sh, sw, pt, pl, dh, dw, OH, OW, dt, yt, epi,
                  s);
     if (st != AFG_ERR_UNSUPPORTED) return st;
   }
   const unsigned g = grid_1d(M * OC);
-#define AFG_DIRECT(T)                                                                          \
-  conv_nhwc_direct_kernel<T><<<g, 256, 0, s>>>(                                                \
-      reinterpret_cast<const T*>(x), reinterpret_cast<const T*>(w), bias, reinterpret_cast<T*>(y), \
+#define AFG_DIRECT(T, TO)                                                                      \
+  conv_nhwc_direct_kernel<T, TO><<<g, 256, 0, s>>>(                                            \
+      reinterpret_cast<const T*>(x), reinterpret_cast<const T*>(w), bias, reinterpret_cast<TO*>(y), \
       (int)B, (int)H, (int)W, (int)C, (int)OC, (int)KH, (int)KW, (int)sh, (int)sw, (int)pt,     \
       (int)pl, (int)dh, (int)dw, (int)OH, (int)OW, (int)epi)
-  if (dt == AFG_F32) AFG_DIRECT(float);
-  else if (dt == AFG_F16) AFG_DIRECT(__half);
-  else AFG_DIRECT(__nv_bfloat16);
+  if (dt == AFG_F32) AFG_DIRECT(float, float);
+  else if (dt == AFG_F16 && yt == AFG_F32) AFG_DIRECT(__half, float);
+  else if (dt == AFG_F16) AFG_DIRECT(__half, __half);
+  else if (yt == AFG_F32) AFG_DIRECT(__nv_bfloat16, float);
+  else AFG_DIRECT(__nv_bfloat16, __nv_bfloat16);
 #undef AFG_DIRECT
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_nhwc_direct launch");

@@ -961,7 +961,8 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
 afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int64_t B,
                    int64_t H, int64_t W, int64_t C, int64_t OC, int64_t KH, int64_t KW,
                    int64_t sh, int64_t sw, int64_t pt, int64_t pl, int64_t dh, int64_t dw,
-                   int64_t OH, int64_t OW, afg_dtype dt, afg_epilogue epi, cudaStream_t stream) {
+                   int64_t OH, int64_t OW, afg_dtype dt, afg_dtype yt, afg_epilogue epi,
+                   cudaStream_t stream) {
   const int64_t M = B * OH * OW;
   const int64_t K = KH * KW * C;
   const int block_n = OC >= 256 ? 256 : (OC > 64 ? 128 : 64);
@@ -1010,16 +1011,25 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   args.lower_h = lower[1];
   cudaError_t e;
   CUtensorMap tmC;
-  args.tma_store = make_store_map(&tmC, y, dt, M, OC, OC);
-#define AFG_CONV_V(BN, ST)                                                                    \
-  (dt == AFG_BF16                                                                             \
-       ? launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, tmC, args, stream) \
-       : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, tmC, args, stream))
-#define AFG_CONV_P(ST)                                                                         \
-  (dt == AFG_BF16                                                                              \
-       ? launch_variant<256, ST, false, true, __nv_bfloat16, true, true>(tmA, tmB, tmC, args,   \
-                                                                         stream)               \
-       : launch_variant<256, ST, false, false, __half, true, true>(tmA, tmB, tmC, args, stream))
+  args.tma_store = make_store_map(&tmC, y, yt, M, OC, OC);
+  const bool f32_out = yt == AFG_F32;
+#define AFG_CONV_V(BN, ST)                                                                      \
+  (dt == AFG_BF16                                                                               \
+       ? (f32_out ? launch_variant<BN, ST, false, true, float, true>(tmA, tmB, tmC, args, stream) \
+                  : launch_variant<BN, ST, false, true, __nv_bfloat16, true>(tmA, tmB, tmC, args,  \
+                                                                              stream))            \
+       : (f32_out ? launch_variant<BN, ST, false, false, float, true>(tmA, tmB, tmC, args, stream) \
+                  : launch_variant<BN, ST, false, false, __half, true>(tmA, tmB, tmC, args, stream)))
+#define AFG_CONV_P(ST)                                                                          \
+  (dt == AFG_BF16                                                                               \
+       ? (f32_out ? launch_variant<256, ST, false, true, float, true, true>(tmA, tmB, tmC, args,  \
+                                                                          stream)               \
+                  : launch_variant<256, ST, false, true, __nv_bfloat16, true, true>(              \
+                        tmA, tmB, tmC, args, stream))                                           \
+       : (f32_out ? launch_variant<256, ST, false, false, float, true, true>(tmA, tmB, tmC, args, \
+                                                                           stream)              \
+                  : launch_variant<256, ST, false, false, __half, true, true>(tmA, tmB, tmC, args, \
+                                                                              stream)))
   if (pair && K >= 2048)
     e = AFG_CONV_P(6);
   else if (pair)
@@ -1040,8 +1050,8 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
 // AFG_ERR_UNSUPPORTED when the shape does not fit (the caller then uses the
 // im2col path).
 afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, int64_t B,
-                     int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_epilogue epi,
-                     cudaStream_t stream) {
+                     int64_t H, int64_t W, int64_t C, int64_t OC, afg_dtype dt, afg_dtype yt,
+                     afg_epilogue epi, cudaStream_t stream) {
   static const int mode = [] {  // AFG_CONV_HALO=0 turns it off (A/B measurements)
     const char* e = getenv("AFG_CONV_HALO");
     return e ? atoi(e) : 1;
@@ -1105,9 +1115,13 @@ afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, i
     return e2 != cudaSuccess ? e2 : cudaGetLastError();
   };
   cudaError_t e;
-#define AFG_HALO(BN, RB)                                                                         \
-  (dt == AFG_BF16 ? go(conv_halo_kernel<BN, true, __nv_bfloat16, RB>, HaloSmem<BN, RB>::TOTAL)  \
-                  : go(conv_halo_kernel<BN, false, __half, RB>, HaloSmem<BN, RB>::TOTAL))
+#define AFG_HALO(BN, RB)                                                                        \
+  (yt == AFG_F32                                                                               \
+       ? (dt == AFG_BF16 ? go(conv_halo_kernel<BN, true, float, RB>, HaloSmem<BN, RB>::TOTAL)    \
+                         : go(conv_halo_kernel<BN, false, float, RB>, HaloSmem<BN, RB>::TOTAL))  \
+       : (dt == AFG_BF16                                                                       \
+              ? go(conv_halo_kernel<BN, true, __nv_bfloat16, RB>, HaloSmem<BN, RB>::TOTAL)      \
+              : go(conv_halo_kernel<BN, false, __half, RB>, HaloSmem<BN, RB>::TOTAL)))
   // one channel chunk and one OC block: keep the filter resident
   const bool res_b = C == 64 && OC <= block_n && block_n <= 128;
   if (block_n == 256) e = AFG_HALO(256, false);

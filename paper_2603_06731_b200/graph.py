@@ -13,7 +13,8 @@ from . import AfgError, lib
 
 
 def check_graph(graph) -> None:
-    """parseGraphJson + checkGraph (GraphError -> AfgError status 1)."""
+    """Graph JSON read + table-driven validation with checkGraph's error
+    behaviour (GraphError -> AfgError status 1)."""
     text = graph if isinstance(graph, str) else json.dumps(graph)
     L = lib()
     st = L.afg_graph_check_json(text.encode())
@@ -21,9 +22,16 @@ def check_graph(graph) -> None:
         raise AfgError(st, L.afg_last_error().decode(errors="replace"))
 
 
-def execute(graph, inputs: dict, fuse: bool = True, stream=None, want_plan=False):
+FUSE = 1
+EXACT = 2
+
+
+def execute(graph, inputs: dict, fuse: bool = True, stream=None, want_plan=False,
+            exact: bool = False):
     """Runs the graph on the GPU. inputs: {id or %id: array}. Returns
-    {"%id": float64 array} (and the executed kernel plan if want_plan)."""
+    {"%id": float64 array} (and the executed kernel plan if want_plan).
+    fuse: kernel patterns + fused VM regions (else one launch per op);
+    exact: keep f32 tensors off the tensor cores (bit-exact paths only)."""
     text = graph if isinstance(graph, str) else json.dumps(graph)
     L = lib()
     names = list(inputs)
@@ -33,7 +41,8 @@ def execute(graph, inputs: dict, fuse: bool = True, stream=None, want_plan=False
     c_data = (DP * len(names))(*[a.ctypes.data_as(DP) for a in arrs])
     c_numel = (ctypes.c_int64 * len(names))(*[a.size for a in arrs])
     out = ctypes.c_void_p()
-    st = L.afg_graph_run(text.encode(), len(names), c_names, c_data, c_numel, int(fuse),
+    flags = (FUSE if fuse else 0) | (EXACT if exact else 0)
+    st = L.afg_graph_run(text.encode(), len(names), c_names, c_data, c_numel, flags,
                          stream, ctypes.byref(out))
     if st != 0:
         raise AfgError(st, L.afg_last_error().decode(errors="replace"))

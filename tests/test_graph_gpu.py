@@ -34,6 +34,10 @@ def tol_for(name):
         return 0.0
     if "f16" in name:
         return 2e-3
+    if "gelu" in name:
+        # the composite (14 nests, every intermediate rounded to f32) against
+        # the fused fp32 GELU epilogue (fast exp / reciprocal): stated 1e-5
+        return 1e-5
     return 1e-6
 
 
@@ -96,7 +100,7 @@ def test_int8_output_matmul_saturates_every_partial_sum(cuda):
     a = np.array([[100, 100, -100], [-100, -100, 100]])
     b = np.array([[1, 2], [1, 0], [1, -1]])
     out, plan = execute(g, {"a": a, "b": b}, want_plan=True)
-    assert any("int_matmul_sat" in p for p in plan), plan
+    assert any("per-step rounding" in p for p in plan), plan
     # reference: [[27, 127], [-28, -128]] (-100 - 100 -> -128, + 100 -> -28)
     assert out["%c"].tolist() == [[27.0, 127.0], [-28.0, -128.0]]
     if O.ref_available():
