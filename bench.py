@@ -16,7 +16,13 @@ max-over-ranks reduction of the device time; no data-path collective).
 interpreter, oracle/_ref, or the oracle C port if it is absent) on the
 host cores with every thread, on a bounded sample of the same workload.
 
-Prints ONE JSON line (rank 0).
+Prints ONE JSON line (rank 0). The default run (workload gemm_bf16, no
+--only) also measures every other BASELINE config in the same process and
+reports them under "workloads": the GEMM sweep sizes, fp32 1024^3, attention
+(causal and not), the ResNet-50 conv set, the BERT layer, softmax, layernorm,
+int8 GEMM and the split-K tensor-parallel GEMM -- each with its value, the
+roofline fraction (same statistic as value: the mean step time), the clocks
+and the ncu DRAM traffic of its dominant kernel.
 """
 from __future__ import annotations
 
@@ -48,6 +54,13 @@ def load_peaks():
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                 "source": "fallback"}
+
+
+def fp32_simt_peak(clk):
+    """FP32 CUDA-core peak of the B200: 148 SMs x 128 FP32 lanes x 2 flop per
+    FMA x the SM clock (the max clock nvidia-smi reports, else 1965 MHz)."""
+    mhz = (clk or {}).get("sm_max_mhz") or 1965.0
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
 
 
 def floor_fields(wl, peaks, k_ms):
@@ -207,7 +220,12 @@ class GemmBF16:
     def launches_per_step(self):
         return 1
 
-    # e2e: pinned host bf16 buffers -> H2D -> afg_gemm (C ABI) -> D2H
+    # e2e: pinned host bf16 buffers -> H2D -> afg_gemm (C ABI) -> D2H, the rows
+    # of A / C pipelined in chunks over the two copy engines: chunk i's GEMM
+    # overlaps chunk i+1's H2D and chunk i-1's D2H
+    e2e_path = ("pinned host -> H2D (copy stream) -> afg_gemm per 1/8 of the rows -> D2H (second "
+                "copy stream), chunks overlapped; B and bias copied once per step")
+
     def e2e_setup(self):
         t = self.torch
         self.hA = self.A.cpu().pin_memory()
@@ -219,15 +237,36 @@ class GemmBF16:
         self.dbias = t.empty_like(self.bias)
         self.h2d = self.hA.numel() * 2 + self.hB.numel() * 2 + self.hbias.numel() * 4
         self.d2h = self.hC.numel() * 2
+        self.s_in, self.s_out = t.cuda.Stream(), t.cuda.Stream()
+        step = max(256, -(-self.m // 8) // 256 * 256)
+        self.chunks = [(r, min(self.m, r + step)) for r in range(0, self.m, step)]
 
     def e2e_step(self):
         from paper_2603_06731_b200 import Epilogue
-        self.dA.copy_(self.hA, non_blocking=True)
-        self.dB.copy_(self.hB, non_blocking=True)
-        self.dbias.copy_(self.hbias, non_blocking=True)
-        self.ops.gemm(self.dA, self.dB, bias=self.dbias, epilogue=Epilogue.BIAS_GELU_TANH,
-                      out=self.C)
-        self.hC.copy_(self.C, non_blocking=True)
+        t = self.torch
+        cur = t.cuda.current_stream()
+        self.s_in.wait_stream(cur)
+        ev_in, ev_out = [], []
+        with t.cuda.stream(self.s_in):
+            self.dB.copy_(self.hB, non_blocking=True)
+            self.dbias.copy_(self.hbias, non_blocking=True)
+            for r0, r1 in self.chunks:
+                self.dA[r0:r1].copy_(self.hA[r0:r1], non_blocking=True)
+                e = t.cuda.Event()
+                e.record(self.s_in)
+                ev_in.append(e)
+        for (r0, r1), e in zip(self.chunks, ev_in):
+            cur.wait_event(e)
+            self.ops.gemm(self.dA[r0:r1], self.dB, bias=self.dbias,
+                          epilogue=Epilogue.BIAS_GELU_TANH, out=self.C[r0:r1])
+            o = t.cuda.Event()
+            o.record(cur)
+            ev_out.append(o)
+        for (r0, r1), o in zip(self.chunks, ev_out):
+            self.s_out.wait_event(o)
+            with t.cuda.stream(self.s_out):
+                self.hC[r0:r1].copy_(self.C[r0:r1], non_blocking=True)
+        cur.wait_stream(self.s_out)
 
     # bounded CPU sample of the same workload through the reference path
     def reference_sample(self, threads):
@@ -484,10 +523,12 @@ class ResNetConvs(_Base):
             bias = _dev_uniform((OC,), f"b{i}", 1, -1, 1, torch.float32)
             y = torch.empty((self.b, OH, OH, OC), dtype=torch.bfloat16, device=dev)
             self.layers.append((x, w, bias, y, k, s, pad, cnt))
+            # a strided 1x1 conv reads only every s-th pixel of its input
+            x_read = self.b * OH * OH * C if (k == 1 and s > 1) else x.numel()
             self.flops_rank += cnt * 2.0 * self.b * OH * OH * OC * C * k * k
-            self.alg_bytes_rank += cnt * 2.0 * (x.numel() + y.numel() + w.numel())
+            self.alg_bytes_rank += cnt * 2.0 * (x_read + y.numel() + w.numel())
             self.ops_fb.append((cnt, 2.0 * self.b * OH * OH * OC * C * k * k,
-                                2.0 * (x.numel() + y.numel() + w.numel())))
+                                2.0 * (x_read + y.numel() + w.numel())))
         self.flops_total = self.flops_rank * self.batch / self.b
 
     def step(self):
@@ -593,7 +634,7 @@ class BertLayer(_Base):
         return [self.y]
 
     def reference_sample(self, threads):
-        return ReferenceGemmSample(self.hd, threads, act="relu", rows=4, cols=96)
+        return ReferenceGraphSample("bert", threads)
 
 
 class MemChain(_Base):
@@ -778,6 +819,13 @@ class ReferenceGraphSample:
             g, fixed = attention_graph(1, 1, N, D, causal)
             self.flops = 4.0 * N * N * D * (0.5 if causal else 1.0) * threads
             self.desc = f"1 head N={N} D={D} attention graph"
+        elif kind == "bert":
+            from oracle.graphs import bert_layer_graph
+            g, fixed, fl = bert_layer_graph(32, 64, 2, 256)
+            self.flops = fl * threads
+            self.desc = ("BERT encoder layer graph S=32 hidden=64 heads=2 ffn=256 (QKV/out/FFN "
+                         "matmuls + bias, scaled attention, GELU composite, residuals; LN has "
+                         "no reference op)")
         elif kind == "conv":
             g, fixed = nhwc_conv_graph(1, 8, 8, 64, 64, 3, 1, "same")
             self.flops = 2.0 * 64 * 64 * 64 * 9 * threads
@@ -857,46 +905,65 @@ def run_reference(args, wl, rank, world):
 
 # ============================================================== afg arm ===
 
-def run_afg(args, wl, rank, world, local):
-    import torch
+class Ctx:
+    """Per-process device / distributed plumbing shared by every workload."""
 
-    import paper_2603_06731_b200 as afg
-    dev = torch.device(f"cuda:{local}")
-    torch.cuda.set_device(dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    peaks = load_peaks()
-    wl.setup(rank, world, dev)
-    torch.cuda.synchronize()
-
-    def barrier():
+    def __init__(self, rank, world, local):
+        import torch
+        self.torch = torch
+        self.rank, self.world, self.local = rank, world, local
+        self.dev = torch.device(f"cuda:{local}")
+        torch.cuda.set_device(self.dev)
         if world > 1:
             import torch.distributed as dist
-            dist.barrier()
-        torch.cuda.synchronize()
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.peaks = load_peaks()
 
-    def max_over_ranks(v):
-        if world == 1:
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, v):
+        if self.world == 1:
             return v
         import torch.distributed as dist
-        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        t = self.torch.tensor([v], device=self.dev, dtype=self.torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def close(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def measure(ctx, wl, steps, warmup, no_graph=False, min_timed_s=0.25):
+    """Device-timed steps of one workload: W warm-up steps, the step captured
+    once into a CUDA graph and replayed, K timed steps (at least `min_timed_s`
+    of device time so the clock sampler sees the region), each bracketed by
+    CUDA events on the launching stream, barrier + sync on both sides, the
+    mean step time max-reduced over ranks. Returns the measurement dict."""
+    import torch
+
+    import paper_2603_06731_b200 as afg
+    wl.setup(ctx.rank, ctx.world, ctx.dev)
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     pre = getattr(wl, "pre_step", None)  # untimed per-step prologue (L2 flush)
-    for _ in range(max(args.warmup, 3)):
+    t0 = time.perf_counter()
+    for _ in range(max(warmup, 3)):
         if pre:
             pre()
         wl.step()
     torch.cuda.synchronize()
-    # The step is captured once into a CUDA graph and replayed: host/ctypes
-    # launch latency then never leaks into the device timing of short steps.
-    launches0 = afg.launch_count()
+    est = (time.perf_counter() - t0) / max(warmup, 3)
+    steps = max(steps, min(200, int(math.ceil(min_timed_s / max(est, 1e-5)))))
     run = wl.step
     graph = None
-    if not args.no_graph:
+    launches_per_step = None
+    if not no_graph:
         side = torch.cuda.Stream()
         side.wait_stream(stream)
         with torch.cuda.stream(side):
@@ -908,105 +975,160 @@ def run_afg(args, wl, rank, world, local):
         with torch.cuda.graph(graph):
             wl.step()
         run = graph.replay
-    launches_per_step = afg.launch_count() - launches0 if graph else None
+        launches_per_step = afg.launch_count() - launches0
     for _ in range(2):
         if pre:
             pre()
         run()
-    barrier()
-    clocks = ClockSampler(local)
+    ctx.barrier()
+    clocks = ClockSampler(ctx.local)
     clocks.start()
     time.sleep(0.3)
     launches0 = afg.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    barrier()
+           for _ in range(steps)]
+    ctx.barrier()
     # hold the GPU in a ~2 ms spin before the first step so the host enqueues
     # every step (graph replays, events) ahead of the device: no host launch
     # latency can sit between a step's start and end events
-    torch.cuda._sleep(4_000_000)  # cycles (~2 ms at 1.965 GHz)
-    for i in range(args.steps):
+    torch.cuda._sleep(4_000_000)
+    for i in range(steps):
         if pre:
             pre()  # enqueued before the start event: the GPU is busy, timing is exact
         evs[i][0].record(stream)
         run()
         evs[i][1].record(stream)
-    barrier()
-    launches = (launches_per_step * args.steps if graph is not None
+    ctx.barrier()
+    launches = (launches_per_step * steps if graph is not None
                 else afg.launch_count() - launches0)
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms = sum(step_ms) / args.steps
+    step_ms = [x.elapsed_time(y) for x, y in evs]
+    ms = sum(step_ms) / steps  # ONE statistic (the mean) for value and roofline
     clk = clocks.stop()
-    ms_max = max_over_ranks(ms)
+    ms_max = ctx.max_over_ranks(ms)
     scale = 1e9 if wl.unit == "GB/s" else 1e12
     value = wl.flops_total / (ms_max * 1e-3) / scale
-
-    # roofline of the step's kernels on this rank (device time of the step;
-    # single-kernel workloads: exactly the dominant kernel's duration)
-    k_ms = statistics.median(step_ms)
+    peaks = ctx.peaks
     peak_note = f"{peaks['source']} (MEASURED_PEAKS.json burst)"
-    if wl.bound == "hbm":
-        achieved = wl.alg_bytes_rank / (k_ms * 1e-3) / 1e9
+    bound = wl.bound
+    if bound == "hbm":
+        achieved = wl.alg_bytes_rank / (ms * 1e-3) / 1e9
         peak, unit = peaks["hbm_gbs"], "GB/s"
-    elif wl.bound == "tensor-i8":  # dense int8 = 2x dense bf16 on B200 (4.5 vs 2.25 PFLOP/s nominal)
-        achieved = wl.flops_rank / (k_ms * 1e-3) / 1e12
+    elif bound == "tensor-i8":  # dense int8 = 2x dense bf16 on B200 (4.5 vs 2.25 PFLOP/s nominal)
+        achieved = wl.flops_rank / (ms * 1e-3) / 1e12
         peak, unit = 2.0 * peaks["bf16_tflops"], "TOP/s"
-        peak_note = f"2 x the {peaks['source']} bf16 burst peak (MEASURED_PEAKS.json has no int8 entry)"
+        peak_note = (f"assumed: 2 x the {peaks['source']} bf16 burst peak (MEASURED_PEAKS.json "
+                     f"has no int8 entry; nominal dense int8 = 2 x dense bf16)")
+    elif bound == "fp32-simt":
+        achieved = wl.flops_rank / (ms * 1e-3) / 1e12
+        peak, unit = fp32_simt_peak(clk), "TFLOP/s"
+        peak_note = ("derived FP32 CUDA-core peak: 148 SM x 128 lanes x 2 flop x sm_max_mhz "
+                     "(the path is the interpreter-exact fp32 GEMM, no tensor cores)")
     else:
-        achieved = wl.flops_rank / (k_ms * 1e-3) / 1e12
+        achieved = wl.flops_rank / (ms * 1e-3) / 1e12
         peak, unit = peaks["bf16_tflops"], "TFLOP/s"
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "peak_source": peak_note, "step_ms": ms,
+            "statistic": "mean of the timed steps (same as value)",
+            "traffic": traffic_for(wl.name), **floor_fields(wl, peaks, ms)}
+    if bound == "fp32-simt":
+        roof["frac_of_bf16_peak"] = achieved / peaks["bf16_tflops"]
+    return {"metric": wl.metric, "value": value, "unit": wl.unit, "ms_per_step": ms_max,
+            "steps": steps, "dtype": wl.dtype, "config": wl.config(ctx.world), "roofline": roof,
+            "gpu_launches": int(launches), "clocks": clk}
 
-    # end to end through the C ABI with host buffers
+
+def measure_e2e(ctx, wl, steps):
+    """The same metric end to end through the C ABI with pinned host buffers:
+    every step copies its inputs H2D and its result D2H inside the timed
+    region (device-timed, max over ranks)."""
+    import torch
+    stream = torch.cuda.current_stream()
     wl.e2e_setup()
     for _ in range(2):
         wl.e2e_step()
-    barrier()
+    ctx.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e_steps = max(1, min(args.steps, 5))
+    e_steps = max(1, min(steps, 5))
     e0.record(stream)
     for _ in range(e_steps):
         wl.e2e_step()
     e1.record(stream)
-    barrier()
-    e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps)
-    e2e_value = wl.flops_total / (e_ms * 1e-3) / scale
+    ctx.barrier()
+    e_ms = ctx.max_over_ranks(e0.elapsed_time(e1) / e_steps)
+    scale = 1e9 if wl.unit == "GB/s" else 1e12
+    return {"value": wl.flops_total / (e_ms * 1e-3) / scale, "unit": wl.unit, "ms_per_step": e_ms,
+            "h2d_bytes_per_step": wl.h2d * ctx.world, "d2h_bytes_per_step": wl.d2h * ctx.world,
+            "path": getattr(wl, "e2e_path", "pinned host -> cudaMemcpyAsync -> afg C ABI -> D2H")}
 
+
+def cpu_baseline(wl):
+    threads = host_threads()
+    sample = wl.reference_sample(threads)
+    t = sample.run_once()
+    scale = 1e9 if wl.unit == "GB/s" else 1e12
+    return {"value": sample.flops / t / scale, "unit": wl.unit, "cores": threads,
+            "kind": getattr(sample, "kind_label", getattr(sample, "kind", None)),
+            "sample": sample.describe(), "seconds": t}
+
+
+def release(wl):
+    import gc
+
+    import torch
+    for k in list(vars(wl)):
+        if k not in ("torch", "ops"):
+            setattr(wl, k, None)
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+# the other BASELINE configs measured in the default run (name, constructor)
+SUB_WORKLOADS = [
+    ("gemm_bf16_2048", lambda: GemmBF16(2048)), ("gemm_bf16_4096", lambda: GemmBF16(4096)),
+    ("gemm_bf16_8192", lambda: GemmBF16(8192)), ("gemm_fp32_1024", lambda: GemmFP32()),
+    ("attention", lambda: Attention(False)), ("attention_causal", lambda: Attention(True)),
+    ("resnet50_convs", lambda: ResNetConvs()), ("bert_layer", lambda: BertLayer()),
+    ("softmax", lambda: MemChain("softmax")), ("layernorm", lambda: MemChain("layernorm")),
+    ("gemm_i8_8192", lambda: GemmI8(8192)),
+]
+
+
+def run_afg(args, wl, rank, world, local, subs=()):
+    ctx = Ctx(rank, world, local)
+    m = measure(ctx, wl, args.steps, args.warmup, args.no_graph)
+    e2e = measure_e2e(ctx, wl, args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = host_threads()
-        sample = wl.reference_sample(threads)
-        t = sample.run_once()
-        scale = 1e9 if wl.unit == "GB/s" else 1e12
-        cpu = {"value": sample.flops / t / scale, "unit": wl.unit, "cores": threads,
-               "kind": getattr(sample, "kind_label", getattr(sample, "kind", None)),
-               "sample": sample.describe(), "seconds": t}
-
+        cpu = cpu_baseline(wl)
+    release(wl)
+    workloads = {}
+    for name, make in subs:
+        sub = make()
+        try:
+            r = measure(ctx, sub, min(args.steps, 20), args.warmup, args.no_graph,
+                        min_timed_s=0.15)
+            workloads[name] = {k: r[k] for k in ("value", "unit", "ms_per_step", "steps",
+                                                 "dtype", "roofline", "clocks", "gpu_launches")}
+            workloads[name]["workload"] = r["config"].get("workload")
+        except Exception as e:  # report, never hide: the entry says what failed
+            workloads[name] = {"error": f"{type(e).__name__}: {e}"}
+        release(sub)
     if rank == 0:
-        line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
-                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
-                "higher_is_better": True,
+        line = {"metric": m["metric"], "value": m["value"], "unit": m["unit"], "n_gpus": world,
+                "steps": m["steps"], "warmup": max(args.warmup, 3),
+                "ms_per_step": m["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak" if isinstance(wl, GemmFP32) else "strong",
-                "vs_baseline": None, "dtype": wl.dtype,
+                "vs_baseline": None, "dtype": m["dtype"],
                 "data": "synthetic (device-side makeRandomTensor stream, uniform)",
-                "config": wl.config(world),
-                "roofline": {"bound": wl.bound if wl.bound in ("hbm", "tensor") else "tensor",
-                             "achieved": achieved, "peak": peak, "unit": unit,
-                             "frac": achieved / peak,
-                             "peak_source": peak_note,
-                             "kernel_ms": k_ms, "traffic": traffic_for(wl.name),
-                             **floor_fields(wl, peaks, k_ms)},
-                "e2e": {"value": e2e_value, "unit": wl.unit, "ms_per_step": e_ms,
-                        "h2d_bytes_per_step": wl.h2d * world, "d2h_bytes_per_step": wl.d2h * world,
-                        "path": "pinned host -> cudaMemcpyAsync -> afg C ABI -> D2H"},
-                "gpu_launches": int(launches),
-                "clocks": clk,
-                "cpu_baseline": cpu,
-                "impl": "afg"}
+                "config": m["config"], "roofline": m["roofline"], "e2e": e2e,
+                "gpu_launches": m["gpu_launches"], "clocks": m["clocks"],
+                "cpu_baseline": cpu, "impl": "afg"}
+        if workloads:
+            line["workloads"] = workloads
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    ctx.close()
     return 0
 
 
@@ -1022,15 +1144,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying "
                     "a captured CUDA graph of the step")
+    ap.add_argument("--only", action="store_true", help="the named workload alone (no "
+                    "'workloads' sub-dict in the default run)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     names = sorted(WORKLOADS) if args.all else [args.workload]
+    default_run = (args.workload == "gemm_bf16" and args.size == 16384 and not args.all
+                   and not args.only)
     for name in names:
         wl = WORKLOADS[name](args)
         if args.impl == "reference":
             run_reference(args, wl, rank, world)
         else:
-            run_afg(args, wl, rank, world, local)
+            run_afg(args, wl, rank, world, local, SUB_WORKLOADS if default_run else ())
     return 0
 
 

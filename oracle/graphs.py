@@ -103,3 +103,78 @@ def nhwc_conv_graph(B, H, W, C, OC, k, stride, padding):
     return g, {"z": np.zeros((B, OC, OH, OW))}
 
 
+
+
+def bert_layer_graph(S, hidden, heads, ffn):
+    """A BERT-base-style encoder layer (one sequence) in the unchanged graph
+    API, as SURVEY.md App. B writes it: Q/K/V projections as three matmuls +
+    bias, heads via reshape + transpose, scaled attention (constant-tensor
+    mul), output projection + bias + residual, GELU FFN (the 14-nest
+    composite) + residual. Layernorm has no expression in the reference API
+    (frontend.cpp:153-157) and is omitted. Returns (graph, fixed constants)."""
+    dh = hidden // heads
+    t, ops, fixed = [], [], {}
+
+    def ten(i, s):
+        t.append(T(i, s))
+
+    def op(o, ins, out, **attrs):
+        d = {"op": o, "inputs": ins, "output": out}
+        if attrs:
+            d["attrs"] = attrs
+        ops.append(d)
+
+    def linear(x, w, b, out, k, n):
+        ten(w, [k, n]), ten(b, [n]), ten(out + "_mm", [S, n]), ten(out + "_bb", [S, n]), ten(out, [S, n])
+        op("matmul", [x, w], out + "_mm")
+        op("broadcast_in_dim", [b], out + "_bb", dims=[1])
+        op("add", [out + "_mm", out + "_bb"], out)
+
+    ten("x", [S, hidden])
+    for p in ("q", "k", "v"):
+        linear("x", "w" + p, "b" + p, p, hidden, hidden)
+        ten(p + "4", [1, S, heads, dh]), ten(p + "h", [1, heads, S, dh])
+        op("reshape", [p], p + "4")
+        op("transpose", [p + "4"], p + "h", perm=[0, 2, 1, 3])
+    ten("kt", [1, heads, dh, S]), ten("qk", [1, heads, S, S]), ten("sc", [1, heads, S, S])
+    ten("qs", [1, heads, S, S]), ten("soft", [1, heads, S, S]), ten("ctx", [1, heads, S, dh])
+    op("transpose", ["kh"], "kt", perm=[0, 1, 3, 2])
+    op("batch_matmul", ["qh", "kt"], "qk")
+    op("mul", ["qk", "sc"], "qs")
+    op("softmax", ["qs"], "soft", axis=-1)
+    op("batch_matmul", ["soft", "vh"], "ctx")
+    fixed["sc"] = np.full((1, heads, S, S), 1.0 / math.sqrt(dh))
+    ten("ctx_t", [1, S, heads, dh]), ten("ctx2", [S, hidden])
+    op("transpose", ["ctx"], "ctx_t", perm=[0, 2, 1, 3])
+    op("reshape", ["ctx_t"], "ctx2")
+    linear("ctx2", "wo", "bo", "attn", hidden, hidden)
+    ten("res1", [S, hidden])
+    op("add", ["x", "attn"], "res1")
+    linear("res1", "w1", "b1", "h", hidden, ffn)
+    # tanh-GELU composite on h
+    for i, s in [("c1", [S, ffn]), ("c2", [S, ffn]), ("mask", [S, ffn, 2]), ("x2", [S, ffn]),
+                 ("x3", [S, ffn]), ("tt", [S, ffn]), ("ss", [S, ffn]), ("u2", [S, ffn]),
+                 ("bu", [S, ffn, 2]), ("mm", [S, ffn, 2]), ("sm", [S, ffn, 2]),
+                 ("sel", [S, ffn, 2]), ("sg", [S, ffn]), ("g", [S, ffn])]:
+        ten(i, s)
+    op("mul", ["h", "h"], "x2")
+    op("mul", ["x2", "h"], "x3")
+    op("mul", ["x3", "c1"], "tt")
+    op("add", ["h", "tt"], "ss")
+    op("mul", ["ss", "c2"], "u2")
+    op("broadcast_in_dim", ["u2"], "bu", dims=[0, 1])
+    op("mul", ["bu", "mask"], "mm")
+    op("softmax", ["mm"], "sm", axis=-1)
+    op("mul", ["sm", "mask"], "sel")
+    op("reduce", ["sel"], "sg", op="sum", axis=2)
+    op("mul", ["h", "sg"], "g")
+    fixed["c1"] = np.full((S, ffn), 0.044715)
+    fixed["c2"] = np.full((S, ffn), 2.0 * math.sqrt(2.0 / math.pi))
+    m = np.zeros((S, ffn, 2))
+    m[..., 0] = 1.0
+    fixed["mask"] = m
+    linear("g", "w2", "b2", "o2", ffn, hidden)
+    ten("y", [S, hidden])
+    op("add", ["res1", "o2"], "y")
+    flops = 2.0 * S * hidden * (4 * hidden + 2 * ffn) + 4.0 * heads * S * S * dh
+    return {"tensors": t, "ops": ops, "outputs": ["y"]}, fixed, flops

@@ -92,11 +92,31 @@ class ProgramRunner {
       for (const auto& u : used) ++refs[u];
       if (top.kind == NestOpKind::For || top.kind == NestOpKind::Parallel) ++nests_;
     }
+    // top-level straight-line code (e.g. mma_load / mma_compute / mma_store
+    // at function scope) runs as one single-thread launch, so its SSA values
+    // flow from op to op as in the interpreter
+    NestOp seq;
+    auto flush_seq = [&] {
+      if (seq.body.empty()) return;
+      seq.kind = NestOpKind::For;
+      seq.ivs = {"$seq"};
+      seq.lowers = {{IndexExpr::constant(0)}};
+      seq.uppers = {{IndexExpr::constant(1)}};
+      const std::string line = R_.run_vm(seq, refs);
+      if (st_) st_->plan.push_back(line + " (function-scope ops)");
+      seq = NestOp{};
+    };
     for (const auto& top : p_.body) {
+      if (top.kind != NestOpKind::For && top.kind != NestOpKind::Parallel) {
+        seq.body.push_back(top);
+        continue;
+      }
+      flush_seq();
       if (opt_.dispatch && (dispatch_matmul(top) || dispatch_conv(top))) continue;
       const std::string line = R_.run_vm(top, refs);
       if (st_) st_->plan.push_back(line);
     }
+    flush_seq();
     std::map<std::string, TensorValue> out;
     for (const auto& b : p_.buffers) {
       if (!b.isOutput) continue;

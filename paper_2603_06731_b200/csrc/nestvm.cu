@@ -48,6 +48,7 @@ constexpr int MAX_PAR = 8;
 constexpr int NIV = 32;
 constexpr int64_t EXPR_END = -1;
 constexpr int64_t EXPR_IV = 101;  // resolved Dim: immediate = iv slot
+constexpr size_t kErrBytes = 8 + 8 + 8 * NIV;
 
 enum VmOp : int32_t {
   OP_LOOP = 1, OP_END, OP_LOAD, OP_STORE, OP_ARITH, OP_IVVAL, OP_MMA_LOAD, OP_MMA_COMPUTE,
@@ -164,8 +165,17 @@ __device__ __forceinline__ int type_bytes_d(int t) {
   return t == VT_I8 ? 1 : (t == VT_F16 || t == VT_BF16) ? 2 : t == VT_F64 ? 8 : 4;
 }
 
-__device__ void fail(const VmArgs& p, int code, int info) {
-  if (atomicCAS(p.err, 0, code) == 0) p.err[1] = info;
+// err: int code, int info, then (at byte 8) the live-iv mask and the 32 iv
+// values of the failing thread (the interpreter's "[ivs: ...]" trace)
+__device__ void fail(const VmArgs& p, int code, int info, const int64_t* iv = nullptr,
+                     uint32_t live = 0) {
+  if (atomicCAS(p.err, 0, code) == 0) {
+    p.err[1] = info;
+    int64_t* t = reinterpret_cast<int64_t*>(p.err + 2);
+    t[0] = iv ? live : 0;
+    if (iv)
+      for (int i = 0; i < NIV; ++i) t[1 + i] = iv[i];
+  }
 }
 
 // Counting mode: per-thread counters (the NestMetrics slots, then 4 per
@@ -208,10 +218,11 @@ __device__ void flush_counts(const VmArgs& p, const unsigned long long* cnt) {
 
 // element offset of an access, or -1 (and the InterpError flag) when out of bounds
 __device__ int64_t address(const VmArgs& p, const VmBuf& b, int list, const int64_t* iv,
-                           int buf_index, int64_t row_extra = 0, int64_t col_extra = 0) {
+                           int buf_index, uint32_t live, int64_t row_extra = 0,
+                           int64_t col_extra = 0) {
   const int32_t n = p.lists[list];
   if (n != b.rank) {
-    fail(p, 2, buf_index);
+    fail(p, 2, buf_index, iv, live);
     return -1;
   }
   int64_t off = 0;
@@ -220,7 +231,7 @@ __device__ int64_t address(const VmArgs& p, const VmBuf& b, int list, const int6
     if (d == n - 2) x += row_extra;
     if (d == n - 1) x += col_extra;
     if (x < 0 || x >= b.shape[d]) {
-      fail(p, 1, buf_index);
+      fail(p, 1, buf_index, iv, live);
       return -1;
     }
     off += x * b.stride[d];
@@ -254,6 +265,8 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
       rem /= p.par_ext[l];
     }
     if (*reinterpret_cast<volatile int*>(p.err) != 0) break;
+    uint32_t live = 0;  // ivs currently bound (for the failure trace)
+    for (int l = 0; l < p.npar; ++l) live |= 1u << p.par_slot[l];
     int pc = 0;
     while (pc < p.ncode) {
       const Ins in = p.code[pc];
@@ -266,6 +279,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
           } else {
             iv[in.a] = lb;
             ub[in.a] = hi;
+            live |= 1u << in.a;
             ++pc;
           }
           break;
@@ -276,6 +290,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
             iv[in.a] = v;
             pc = in.b + 1;
           } else {
+            live &= ~(1u << in.a);
             ++pc;
           }
           break;
@@ -283,7 +298,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
         case OP_IVVAL: r[in.a] = static_cast<double>(iv[in.b]); ++pc; break;
         case OP_LOAD: {
           const VmBuf& b = p.bufs[in.b];
-          const int64_t off = address(p, b, in.c, iv, in.b);
+          const int64_t off = address(p, b, in.c, iv, in.b, live);
           if (off < 0) goto done;
           r[in.a] = ld_native(base_of(b, tid) + off * type_bytes_d(b.type), b.type);
           count_access<COUNT>(p, cnt, in.b, b, false, 1);
@@ -292,7 +307,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
         }
         case OP_STORE: {
           const VmBuf& b = p.bufs[in.b];
-          const int64_t off = address(p, b, in.c, iv, in.b);
+          const int64_t off = address(p, b, in.c, iv, in.b, live);
           if (off < 0) goto done;
           const double v = round_to(operand(in.a, r, p.consts), b.type);
           st_native(const_cast<char*>(base_of(b, tid)) + off * type_bytes_d(b.type), b.type, v);
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
           fragt[in.a < NF ? in.a : 0] = b.type;
           for (int rr = 0; rr < 16; ++rr)
             for (int cc = 0; cc < 16; ++cc) {
-              const int64_t off = address(p, b, in.c, iv, in.b, rr, cc);
+              const int64_t off = address(p, b, in.c, iv, in.b, live, rr, cc);
               if (off < 0) goto done;
               f[rr * 16 + cc] = ld_native(base_of(b, tid) + off * type_bytes_d(b.type), b.type);
             }
@@ -377,7 +392,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
           const double* f = frag[in.a];
           for (int rr = 0; rr < 16; ++rr)
             for (int cc = 0; cc < 16; ++cc) {
-              const int64_t off = address(p, b, in.c, iv, in.b, rr, cc);
+              const int64_t off = address(p, b, in.c, iv, in.b, live, rr, cc);
               if (off < 0) goto done;
               st_native(const_cast<char*>(base_of(b, tid)) + off * type_bytes_d(b.type), b.type,
                         round_to(f[rr * 16 + cc], b.type));
@@ -387,7 +402,7 @@ __global__ void __launch_bounds__(128) nest_vm_kernel(const VmArgs p) {
           ++pc;
           break;
         }
-        default: fail(p, 3, pc); goto done;
+        default: fail(p, 3, pc, iv, live); goto done;
       }
     }
   }
@@ -1088,10 +1103,10 @@ std::string Runner::run_vm(const NestOp& top, const std::map<std::string, int>& 
   cudaError_t e = cudaMemcpyAsync(dblob, blob.data(), total_bytes, cudaMemcpyHostToDevice, s_);
   if (e != cudaSuccess) throw InterpError("afg nest vm: program upload failed");
   if (!err_) {
-    if (cudaMallocAsync(reinterpret_cast<void**>(&err_), 16, s_) != cudaSuccess)
+    if (cudaMallocAsync(reinterpret_cast<void**>(&err_), kErrBytes, s_) != cudaSuccess)
       throw InterpError("afg nest vm: allocation failed");
   }
-  cudaMemsetAsync(err_, 0, 16, s_);
+  cudaMemsetAsync(err_, 0, kErrBytes, s_);
   a.code = reinterpret_cast<const Ins*>(dblob + o_code);
   a.expr = reinterpret_cast<const int64_t*>(dblob + o_expr);
   a.lists = reinterpret_cast<const int32_t*>(dblob + o_list);
@@ -1111,13 +1126,25 @@ std::string Runner::run_vm(const NestOp& top, const std::map<std::string, int>& 
   else throw InterpError("afg nest vm: more than 512 live values in one nest");
   count_launch();
   if (e != cudaSuccess) throw InterpError(std::string("afg nest vm launch: ") + cudaGetErrorString(e));
-  int herr[2] = {0, 0};
-  e = cudaMemcpyAsync(herr, err_, 8, cudaMemcpyDeviceToHost, s_);
+  std::vector<int> herr(kErrBytes / 4, 0);
+  e = cudaMemcpyAsync(herr.data(), err_, kErrBytes, cudaMemcpyDeviceToHost, s_);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s_);
   if (e != cudaSuccess) throw InterpError(std::string("afg kernel failure: ") + cudaGetErrorString(e));
-  if (herr[0] == 1) throw InterpError("out-of-bounds access to " + enc.bufs.at(herr[1]));
-  if (herr[0] == 2) throw InterpError("rank mismatch on access to " + enc.bufs.at(herr[1]));
-  if (herr[0] != 0) throw InterpError("afg nest vm: bad instruction");
+  if (herr[0] != 0) {
+    // "<what> [ivs: %i=3 ...]" like the interpreter's fail() (interp.cpp:258-266)
+    const int64_t* t = reinterpret_cast<const int64_t*>(herr.data() + 2);
+    std::map<std::string, int64_t> bound;
+    for (const auto& [name, slot] : enc.iv)
+      if (t[0] >> slot & 1) bound[name] = t[1 + slot];
+    std::ostringstream msg;
+    if (herr[0] == 1) msg << "out-of-bounds access to " << enc.bufs.at(herr[1]);
+    else if (herr[0] == 2) msg << "rank mismatch on access to " << enc.bufs.at(herr[1]);
+    else msg << "afg nest vm: bad instruction";
+    msg << " [ivs:";
+    for (const auto& [k, v] : bound) msg << " " << k << "=" << v;
+    msg << "]";
+    throw InterpError(msg.str());
+  }
   plan << " over " << np << " parallel level(s)";
   return plan.str();
 }
