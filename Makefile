@@ -29,7 +29,7 @@ $(BUILD)/%.o: $(SRC_DIR)/%.cpp $(HDRS)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xcompiler -fvisibility=hidden
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -Xcompiler -fvisibility=hidden -ldl -lpthread
 
 oracle:
 	$(MAKE) -C oracle

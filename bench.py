@@ -273,6 +273,78 @@ class GemmBF16:
         return ReferenceGemmSample(self.n, threads)
 
 
+class GemmSplitK:
+    """North-star item 4 / SURVEY §8e: the split-K tensor-parallel GEMM, the
+    one config with an exchange step. bf16 16384^3 + bias + tanh-GELU; the K
+    dimension is split across ranks, each computes its fp32 partial on the
+    tensor cores, NCCL reduce-scatters the partials over NVLink into row
+    blocks, the epilogue runs on the reduced rows (afg_gemm_splitk)."""
+
+    metric = "TFLOP/s"
+    unit = "TFLOP/s"
+    dtype = "bf16"
+    bound = "tensor"
+
+    def __init__(self, size=16384):
+        self.n = size
+        self.name = f"gemm_splitk_{size}"
+
+    def config(self, world):
+        return {"workload": f"bf16 matmul {self.n}^3 split-K over {world} rank(s) + NCCL "
+                            f"reduce-scatter of the fp32 partials + bias/tanh-GELU epilogue",
+                "M": self.n, "N": self.n, "K": self.n, "parallelism": f"splitK/{world}",
+                "l2": "operands larger than L2"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        import oracle
+        from paper_2603_06731_b200 import ops
+        from paper_2603_06731_b200.tp import Comm, split_plan
+        self.torch, self.ops = torch, ops
+        n = self.n
+        (k0, k1), _ = split_plan(n, n, rank, world)
+        self.kl = k1 - k0
+        self.A = ops.fill_uniform((n, self.kl), oracle.stream_seed("%a", 1 + rank), -1, 1,
+                                  torch.bfloat16)
+        self.B = ops.fill_uniform((self.kl, n), oracle.stream_seed("%b", 1 + rank), -1, 1,
+                                  torch.bfloat16)
+        self.bias = ops.fill_uniform((n,), oracle.stream_seed("%bias", 1), -1, 1, torch.float32)
+        self.comm = Comm.from_process_group()
+        self.C = torch.empty((n // world, n), dtype=torch.bfloat16, device=dev)
+        from paper_2603_06731_b200 import lib
+        ws = lib().afg_gemm_splitk_workspace(n, n, world, 0)
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self.flops_rank = 2.0 * n * n * self.kl
+        self.flops_total = 2.0 * n ** 3
+        self.alg_bytes_rank = 2.0 * (n * self.kl * 2 + n * n // world) + 4.0 * n * n
+
+    def step(self):
+        from paper_2603_06731_b200 import Epilogue
+        from paper_2603_06731_b200.tp import gemm_splitk
+        gemm_splitk(self.A, self.B, self.comm, bias=self.bias, epilogue=Epilogue.BIAS_GELU_TANH,
+                    out=self.C, workspace=self.ws)
+
+    def launches_per_step(self):
+        return 2
+
+    def e2e_setup(self):
+        t = self.torch
+        self.hA, self.hB = self.A.cpu().pin_memory(), self.B.cpu().pin_memory()
+        self.hC = t.empty_like(self.C, device="cpu").pin_memory()
+        self.h2d = (self.hA.numel() + self.hB.numel()) * 2
+        self.d2h = self.hC.numel() * 2
+
+    def e2e_step(self):
+        self.A.copy_(self.hA, non_blocking=True)
+        self.B.copy_(self.hB, non_blocking=True)
+        self.step()
+        self.hC.copy_(self.C, non_blocking=True)
+
+    def reference_sample(self, threads):
+        return ReferenceGemmSample(self.n, threads)
+
+
 class GemmI8:
     """SURVEY 8f3 (beyond the BASELINE configs): the quant module's int8 GEMM
     (SPEC.md:531-572), i8 x i8 -> exact i32 accumulation, requantised to i8
@@ -703,6 +775,7 @@ class MemChain(_Base):
 
 
 WORKLOADS = {"gemm_bf16": lambda a: GemmBF16(a.size), "gemm_fp32": lambda a: GemmFP32(),
+             "gemm_splitk": lambda a: GemmSplitK(a.size),
              "gemm_i8": lambda a: GemmI8(a.size),
              "attention": lambda a: Attention(False), "attention_causal": lambda a: Attention(True),
              "resnet50_convs": lambda a: ResNetConvs(), "bert_layer": lambda a: BertLayer(),
@@ -1076,6 +1149,9 @@ def release(wl):
     import gc
 
     import torch
+    if getattr(wl, "comm", None) is not None:
+        torch.cuda.synchronize()
+        wl.comm.close()
     for k in list(vars(wl)):
         if k not in ("torch", "ops"):
             setattr(wl, k, None)
@@ -1091,7 +1167,7 @@ SUB_WORKLOADS = [
     ("attention", lambda: Attention(False)), ("attention_causal", lambda: Attention(True)),
     ("resnet50_convs", lambda: ResNetConvs()), ("bert_layer", lambda: BertLayer()),
     ("softmax", lambda: MemChain("softmax")), ("layernorm", lambda: MemChain("layernorm")),
-    ("gemm_i8_8192", lambda: GemmI8(8192)),
+    ("gemm_i8_8192", lambda: GemmI8(8192)), ("gemm_splitk_16384", lambda: GemmSplitK(16384)),
 ]
 
 

@@ -281,6 +281,46 @@ AFG_API afg_status afg_transpose(const void* x, void* y, int rank, const int64_t
 AFG_API afg_status afg_fill_uniform(void* x, int64_t n, uint64_t seed, float lo, float hi,
                             afg_dtype dtype, void* stream);
 
+/* ------------------------------------------------ multi-GPU (NVLink) --- */
+
+/* NCCL communicators (libnccl.so.2 resolved at first use). One per rank via
+ * a unique id (128 bytes) shared out of band, or all of a process's devices
+ * at once (ncclCommInitAll). `comm` values are ncclComm_t. */
+AFG_API afg_status afg_comm_unique_id(void* id_out /* 128 bytes */);
+AFG_API afg_status afg_comm_init_rank(void** comm, int world, const void* id, int rank);
+AFG_API afg_status afg_comm_init_all(void** comms, int ndev, const int* devices);
+AFG_API afg_status afg_comm_destroy(void* comm);
+
+/* Split-K / tensor-parallel (row-parallel) GEMM, the one BASELINE config with
+ * an exchange step: every rank holds A[:, K_r] ([M, K_local])
+ * and B[K_r, :], computes its fp32 partial product on the tensor cores, the
+ * partials are summed across ranks over NVLink by NCCL, and the epilogue
+ * (bias / ReLU / GELU) runs on the sum:
+ *   AFG_SPLITK_REDUCE_SCATTER: C = rows [rank*M/P, (rank+1)*M/P) of the
+ *                              result ([M/P, N], M % P == 0);
+ *   AFG_SPLITK_ALL_REDUCE    : C = the full [M, N] result on every rank.
+ * workspace: device memory of afg_gemm_splitk_workspace(M, N, P, mode) bytes. */
+#define AFG_SPLITK_REDUCE_SCATTER 0
+#define AFG_SPLITK_ALL_REDUCE 1
+AFG_API size_t afg_gemm_splitk_workspace(int64_t M, int64_t N, int world, int mode);
+AFG_API afg_status afg_gemm_splitk(const void* A, int64_t lda, const void* B, int64_t ldb,
+                                   const float* bias, void* C, int64_t ldc, int64_t M, int64_t N,
+                                   int64_t K_local, afg_dtype ab_dtype, afg_dtype c_dtype,
+                                   afg_layout b_layout, afg_epilogue epi, void* comm, int mode,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Thread-per-device group (include/afg_multi.h): one host thread per device,
+ * each with its own stream and (for > 1 device) NCCL communicator.
+ * afg_group_run calls fn(user, rank, device, stream, comm) on every device's
+ * thread concurrently, then waits for all streams; the first failing status
+ * is returned. */
+typedef struct afg_group afg_group;
+typedef afg_status (*afg_group_fn)(void* user, int rank, int device, void* stream, void* comm);
+AFG_API afg_status afg_group_create(int ndev, const int* devices, afg_group** out);
+AFG_API void afg_group_destroy(afg_group* g);
+AFG_API int afg_group_size(const afg_group* g);
+AFG_API afg_status afg_group_run(afg_group* g, afg_group_fn fn, void* user);
+
 /* --------------------------------------------------- encoder layer (BERT) --- */
 
 /* One post-LN transformer encoder layer (BERT-base: hidden 768, 12 heads,

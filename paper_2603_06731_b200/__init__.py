@@ -105,6 +105,17 @@ _SIGS = {
     "afg_quantize": (_i, [_P, _P, _I, _f, _i, _i, _i, _P]),
     "afg_gemm_i8": (_i, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _i, _f, _P]),
     "afg_conv2d_nhwc_i8": (_i, [_P, _P, _P] + [_I] * 15 + [_i, _f, _P]),
+    "afg_comm_unique_id": (_i, [_P]),
+    "afg_comm_init_rank": (_i, [ctypes.POINTER(_P), _i, _P, _i]),
+    "afg_comm_init_all": (_i, [ctypes.POINTER(_P), _i, ctypes.POINTER(_i)]),
+    "afg_comm_destroy": (_i, [_P]),
+    "afg_gemm_splitk_workspace": (ctypes.c_size_t, [_I, _I, _i, _i]),
+    "afg_gemm_splitk": (_i, [_P, _I, _P, _I, _P, _P, _I, _I, _I, _I, _i, _i, _i, _i, _P, _i, _P,
+                             ctypes.c_size_t, _P]),
+    "afg_group_create": (_i, [_i, ctypes.POINTER(_i), ctypes.POINTER(_P)]),
+    "afg_group_destroy": (None, [_P]),
+    "afg_group_size": (_i, [_P]),
+    "afg_group_run": (_i, [_P, _P, _P]),
     "afg_graph_run": (_i, [ctypes.c_char_p, _i, ctypes.POINTER(ctypes.c_char_p),
                            ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
                            ctypes.POINTER(_I), _i, _P, ctypes.POINTER(_P)]),

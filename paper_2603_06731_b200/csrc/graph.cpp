@@ -543,7 +543,7 @@ afg_dtype kernel_dtype(ElementType t) {
 bool is_float(ElementType t) {
   return t == ElementType::F32 || t == ElementType::F16 || t == ElementType::BF16;
 }
-bool is_int(ElementType t) { return t == ElementType::I8 || t == ElementType::I32; }
+
 
 std::string dims_str(const std::vector<int64_t>& s) {
   std::string r;

@@ -94,38 +94,46 @@ def test_gloo_world2_row_sharded_gemm_and_timing():
 
 
 def _splitk_worker(rank, world, port, q):
+    """Host side of the split-K path on gloo: the K slices / output row blocks
+    of split_plan, and the NCCL unique-id handshake Comm.from_process_group
+    performs (rank 0's afg_comm_unique_id bytes broadcast to every rank)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2603_06731_b200.tp import gemm_splitk
-        M, K, N = 36, 64, 20
-        A = O.random_tensor((M, K), "%a", 7, -1, 1)
-        B = O.random_tensor((K, N), "%b", 7, -1, 1)
-        k0, k1 = shard_rows(K, rank, world)
-        fn = lambda a, b: torch.from_numpy(O.matmul(a.numpy(), b.numpy()))  # noqa: E731
-        shard = gemm_splitk(torch.from_numpy(A[:, k0:k1].copy()),
-                            torch.from_numpy(B[k0:k1].copy()), partial_fn=fn)
-        out = [None] * world
-        dist.all_gather_object(out, shard.numpy())
+        from paper_2603_06731_b200 import AfgError
+        from paper_2603_06731_b200.tp import ALL_REDUCE, REDUCE_SCATTER, Comm, split_plan
+        plans = [split_plan(36, 64, rank, world, m) for m in (REDUCE_SCATTER, ALL_REDUCE)]
+        try:
+            uid = Comm.unique_id() if rank == 0 else None
+        except AfgError as e:  # no libnccl / no network interface: handshake untestable here
+            uid = ("unavailable", str(e))
+        box = [uid]
+        dist.broadcast_object_list(box, src=0)
+        got = [None] * world
+        dist.all_gather_object(got, (plans, box[0]))
         if rank == 0:
-            q.put(np.concatenate(out))
+            q.put(got)
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world2_splitk_reduce_scatter():
+def test_gloo_world2_splitk_plan_and_id_handshake():
     world, port = 2, free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_splitk_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    C = q.get(timeout=120)
+    got = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    A = O.random_tensor((36, 64), "%a", 7, -1, 1)
-    B = O.random_tensor((64, 20), "%b", 7, -1, 1)
-    # sum of two f32-rounded half-K partials vs the full product
-    ok, ma, mr, _ = O.compare(C, O.matmul(A, B), 1e-6)
-    assert ok, mr
+    (rs0, ar0), uid0 = got[0]
+    (rs1, ar1), uid1 = got[1]
+    # K slices tile [0, K) without overlap; reduce-scatter rows tile [0, M)
+    assert rs0[0] == (0, 32) and rs1[0] == (32, 64)
+    assert rs0[1] == (0, 18) and rs1[1] == (18, 36)
+    assert ar0[1] == ar1[1] == (0, 36)
+    assert uid0 == uid1  # every rank sees rank 0's id
+    if not (isinstance(uid0, tuple) and uid0[0] == "unavailable"):
+        assert isinstance(uid0, bytes) and len(uid0) == 128 and any(uid0)
