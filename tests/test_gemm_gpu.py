@@ -139,14 +139,18 @@ def test_unaligned_bf16_runs_simt_path(cuda):
 def test_splitk_partials_and_epilogue_apply(cuda):
     """The split-K / TP path on one GPU: two K-slice fp32 partials (strided A
     views, lda = K) summed, then the standalone epilogue kernel."""
-    from paper_2603_06731_b200.tp import finish_epilogue
+    from paper_2603_06731_b200 import lib
+    from paper_2603_06731_b200.ops import _ptr, _stream
     M, N, K = 512, 384, 1024
     a, ah = seeded((M, K), "a", 11, dtype=torch.bfloat16)
     b, bh = seeded((K, N), "b", 11, dtype=torch.bfloat16)
     bias, biash = seeded((N,), "bias", 11, dtype=torch.float32)
     p0 = ops.gemm(a[:, : K // 2], b[: K // 2], out_dtype=torch.float32)
     p1 = ops.gemm(a[:, K // 2:], b[K // 2:], out_dtype=torch.float32)
-    c = finish_epilogue(p0 + p1, bias, Epilogue.BIAS_GELU_TANH, torch.bfloat16)
+    acc = p0 + p1
+    c = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    assert lib().afg_epilogue_apply(_ptr(acc), _ptr(bias), None, _ptr(c), M, N, N,
+                                    int(Epilogue.BIAS_GELU_TANH), 0, 2, _stream()) == 0
     want = O.round_to(O.matmul(ah, bh, biash, epi=O.EPI_GELU_TANH, out_t=O.F64), O.BF16)
     check(to_host(c), want, 2.0**-7, "split-K + epilogue")
 
