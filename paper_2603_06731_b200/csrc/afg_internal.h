@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/afg.h"
@@ -45,6 +46,20 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 inline bool valid_dtype(int t) { return t == AFG_F32 || t == AFG_F16 || t == AFG_BF16; }
 // AFG_OK iff a compute-capability-10.x device is current (no CPU fallback).
 afg_status check_device();
+
+
+// Sets a kernel's dynamic shared-memory opt-in once per device (the attribute
+// is per device; `done` is the call site's own bit set, one bit per device).
+template <typename Kern>
+inline cudaError_t ensure_smem_optin(std::atomic<uint64_t>& done, Kern kern, int smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // ---- kernel families (each .cu file) ---------------------------------------
 afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const float* bias,

@@ -225,7 +225,8 @@ afg_status afg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, cons
                      (ldb % 8 == 0) && aligned16(A) && aligned16(B) &&
                      (c_dtype == AFG_F32 || c_dtype == ab_dtype) && M < (1ll << 31) &&
                      N < (1ll << 31) && K < (1ll << 31) &&
-                     (bias == nullptr || aligned16(bias));
+                     (bias == nullptr || aligned16(bias)) && aligned16(C) &&
+                     (residual == nullptr || aligned16(residual)) && ldc % 8 == 0;
   if (tc_ok)
     return gemm_tc(A, lda, B, ldb, bias, residual, C, ldc, M, N, K, ab_dtype, c_dtype, b_layout,
                    epi, s);

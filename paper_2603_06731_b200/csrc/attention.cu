@@ -26,6 +26,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <vector>
 
 #include "afg_internal.h"
 #include "epilogue.cuh"
@@ -54,6 +58,11 @@ struct AttnArgs {
   int causal;
   int o_dtype;
   int head_group;  // unit order: heads per group (see decode)
+  // host-built schedule (attn_schedule): CTA c runs the unit codes
+  // sched[sched_off[c] .. sched_off[c] + sched_cnt[c]), code = bh * n_pairs + qp
+  const int* sched;
+  const int* sched_off;
+  const int* sched_cnt;
   int o_st32;      // 16-bit O rows 32-byte aligned: 256-bit stores
   int dbg;  // profiling aid (AFG_ATTN_DEBUG): 1 = no softmax math, 2 = no MMAs,
            // 3 = MMAs back to back (no softmax dependency)
@@ -178,6 +187,9 @@ __global__ void __launch_bounds__(384, 1)
   // pairs run from the last (heaviest under causal masking) down, all heads of
   // the group per pair (co-resident CTAs share the group's K/V in L2).
   auto unit_of = [&](int u) {
+    if (args.sched) {  // host-balanced list of unit codes
+      return u < args.sched_cnt[blockIdx.x] ? args.sched[args.sched_off[blockIdx.x] + u] : n_units;
+    }
     const int G = static_cast<int>(gridDim.x);
     return u * G + ((u & 1) ? G - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x));
   };
@@ -187,11 +199,17 @@ __global__ void __launch_bounds__(384, 1)
   auto decode = [&](int lin) {
     const int HEAD_GROUP = args.head_group;
     Unit w;
-    const int grp = lin / (HEAD_GROUP * n_pairs);
-    const int gsize = min(HEAD_GROUP, args.BH - grp * HEAD_GROUP);
-    const int off = lin - grp * HEAD_GROUP * n_pairs;
-    const int qp = n_pairs - 1 - off / gsize;
-    w.bh = grp * HEAD_GROUP + off % gsize;
+    int qp;
+    if (args.sched) {
+      w.bh = lin / n_pairs;
+      qp = lin % n_pairs;
+    } else {
+      const int grp = lin / (HEAD_GROUP * n_pairs);
+      const int gsize = min(HEAD_GROUP, args.BH - grp * HEAD_GROUP);
+      const int off = lin - grp * HEAD_GROUP * n_pairs;
+      qp = n_pairs - 1 - off / gsize;
+      w.bh = grp * HEAD_GROUP + off % gsize;
+    }
     w.hh = w.bh % args.H;
     w.bb = w.bh / args.H;
     w.q0 = qp * 2 * BM;
@@ -629,19 +647,99 @@ __global__ void attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ 
   }
 }
 
+// Unit schedule for the persistent grid (built on the host once per shape and
+// device, kept in device memory): heads are taken in groups whose K / V fit
+// comfortably in L2 (co-resident CTAs then share every K / V tile), and
+// inside a group the units are dealt heaviest first to the CTA with the least
+// accumulated work (greedy LPT, cost = KV tiles of the unit + one tile of
+// per-unit overhead). Causal units differ 10x in cost, so the static snake
+// order either broke the grouping (all 128 heads at once: 2-5x the K / V DRAM
+// traffic) or the balance (groups of 16: the slowest CTA 19% over the mean);
+// LPT per group keeps both.
+struct Sched {
+  int* dev = nullptr;  // [units] codes | [grid] offsets | [grid] counts
+  int grid = 0, units = 0;
+};
+
+const Sched& attn_schedule(int BH, int Nq, int Nk, int D, int causal, int grid) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, Sched> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::vector<int> key = {dev, BH, Nq, Nk, D, causal, grid};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int n_pairs = (Nq + 2 * BM - 1) / (2 * BM);
+  const int nkv_all = (Nk + BN - 1) / BN;
+  auto tiles = [&](int first) {
+    return first >= Nq ? 0 : causal ? std::min(nkv_all, (first + BM - 1) / BN + 1) : nkv_all;
+  };
+  // heads per group: K + V of the group <= ~40 MB of L2
+  const int64_t kv_head = 2ll * Nk * D * 2;
+  const int hg = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(BH, (40ll << 20) / kv_head)));
+  std::vector<std::vector<int>> lists(grid);
+  std::vector<double> load(grid, 0.0);
+  for (int g0 = 0; g0 < BH; g0 += hg) {
+    std::vector<std::pair<double, int>> items;
+    for (int bh = g0; bh < std::min(BH, g0 + hg); ++bh)
+      for (int qp = 0; qp < n_pairs; ++qp)
+        items.push_back({tiles(qp * 2 * BM) + tiles(qp * 2 * BM + BM) + 1.0, bh * n_pairs + qp});
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    using E = std::pair<double, int>;
+    std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
+    for (int c = 0; c < grid; ++c) heap.push({load[c], c});
+    for (const auto& [cost, code] : items) {
+      auto [l, c] = heap.top();
+      heap.pop();
+      lists[c].push_back(code);
+      load[c] = l + cost;
+      heap.push({load[c], c});
+    }
+  }
+  std::vector<int> host;
+  std::vector<int> off(grid), cnt(grid);
+  for (int c = 0; c < grid; ++c) {
+    off[c] = static_cast<int>(host.size());
+    cnt[c] = static_cast<int>(lists[c].size());
+    host.insert(host.end(), lists[c].begin(), lists[c].end());
+  }
+  Sched sc;
+  sc.grid = grid;
+  sc.units = static_cast<int>(host.size());
+  host.insert(host.end(), off.begin(), off.end());
+  host.insert(host.end(), cnt.begin(), cnt.end());
+  if (cudaMalloc(&sc.dev, host.size() * sizeof(int)) == cudaSuccess &&
+      cudaMemcpy(sc.dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice) ==
+          cudaSuccess)
+    return cache[key] = sc;
+  cudaGetLastError();
+  return cache[key] = Sched{};
+}
+
 template <int D, bool BF16>
 cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                      const AttnArgs& a, cudaStream_t s) {
+                      AttnArgs a, cudaStream_t s) {
   auto kern = attn_fwd_kernel<D, BF16>;
   constexpr int smem = AttnSmem<D>::TOTAL;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  if (cudaError_t e = ensure_smem_optin(configured, kern, smem); e != cudaSuccess) return e;
   const int units = a.BH * ((a.Nq + 2 * BM - 1) / (2 * BM));
   const unsigned grid = static_cast<unsigned>(std::min(units, num_sms()));  // persistent
+  static const int sched_env = [] {  // AFG_ATTN_SCHED=0: the in-kernel snake order (A/B)
+    const char* e = getenv("AFG_ATTN_SCHED");
+    return e ? atoi(e) : 1;
+  }();
+  a.sched = a.sched_off = a.sched_cnt = nullptr;
+  if (sched_env) {
+    const Sched& sc = attn_schedule(a.BH, a.Nq, a.Nk, D, a.causal, static_cast<int>(grid));
+    if (sc.dev) {
+      a.sched = sc.dev;
+      a.sched_off = sc.dev + sc.units;
+      a.sched_cnt = sc.dev + sc.units + sc.grid;
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(384);

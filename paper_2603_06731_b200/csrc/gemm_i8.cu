@@ -351,13 +351,10 @@ template <bool PAIR, bool IM2COL = false>
 cudaError_t launch_i8(const CUtensorMap& tmA, const CUtensorMap& tmB, const I8Args& a,
                       cudaStream_t stream) {
   constexpr int smem = I8Smem<PAIR>::TOTAL;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<PAIR, IM2COL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // per instantiation, one bit per device
+  if (cudaError_t e = ensure_smem_optin(configured, gemm_i8_kernel<PAIR, IM2COL>, smem);
+      e != cudaSuccess)
+    return e;
   const int tiles = a.nmb * a.nnb;
   const int grid = PAIR ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms());
   cudaLaunchConfig_t cfg = {};

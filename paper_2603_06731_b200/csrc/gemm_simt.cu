@@ -14,6 +14,8 @@
 // single f32 rounding too, frontend.cpp:447-459).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "afg_internal.h"
 #include "epilogue.cuh"
 
@@ -136,6 +138,129 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtArgs a) {
   }
 }
 
+// fp32 fast path (BASELINE configs[0], the interpreter-exact GEMM): 64 x 64
+// tile, 64 threads, an 8 x 8 register block per thread (rows {4ty..4ty+3,
+// 32+4ty..}, columns {4tx..4tx+3, 32+4tx..}: every shared-memory read is a
+// conflict-free or broadcast LDS.128), 16-deep K slabs double-buffered in
+// shared memory with the next slab prefetched into registers. Each output
+// still accumulates k = 0..K-1 in order with one fmaf per k -- the
+// interpreter's round_f32(a*b + c) per store (interp.cpp:335-347) -- so the
+// result stays bit-exact; only the data movement changed (64 FMAs per 4
+// LDS.128 instead of 16 per 8 LDS.32).
+constexpr int FT = 64, FK = 16;
+
+__global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
+  __shared__ __align__(16) float As[2][FK][FT + 4];
+  __shared__ __align__(16) float Bs[2][FK][FT + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 8, ty = tid / 8;
+  const int m0 = blockIdx.y * FT, n0 = blockIdx.x * FT;
+  const int64_t bz = blockIdx.z;
+  const float* A = reinterpret_cast<const float*>(a.A) + bz * a.sA;
+  const float* B = reinterpret_cast<const float*>(a.B) + bz * a.sB;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+  // loaders: thread t reads A row m0+t (16 k), and B row k0 + t/4, 16 columns
+  float ra[FK], rb[16];
+  const int bk = tid / 4, bn = (tid % 4) * 16;
+  auto load = [&](int k0) {
+    const int gm = m0 + tid;
+#pragma unroll
+    for (int q = 0; q < FK / 4; ++q) {
+      const int gk = k0 + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gm < a.M) {
+        if (gk + 3 < a.K) {
+          v = *reinterpret_cast<const float4*>(A + static_cast<int64_t>(gm) * a.lda + gk);
+        } else {
+          const float* p = A + static_cast<int64_t>(gm) * a.lda;
+          v.x = gk < a.K ? p[gk] : 0.f;
+          v.y = gk + 1 < a.K ? p[gk + 1] : 0.f;
+          v.z = gk + 2 < a.K ? p[gk + 2] : 0.f;
+        }
+      }
+      ra[4 * q] = v.x;
+      ra[4 * q + 1] = v.y;
+      ra[4 * q + 2] = v.z;
+      ra[4 * q + 3] = v.w;
+    }
+    const int gk = k0 + bk;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gn = n0 + bn + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gk < a.K && gn < a.N)  // N % 4 == 0 on this path
+        v = *reinterpret_cast<const float4*>(B + static_cast<int64_t>(gk) * a.ldb + gn);
+      rb[4 * q] = v.x;
+      rb[4 * q + 1] = v.y;
+      rb[4 * q + 2] = v.z;
+      rb[4 * q + 3] = v.w;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int k = 0; k < FK; ++k) As[buf][k][tid] = ra[k];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<float4*>(&Bs[buf][bk][bn + 4 * q]) =
+          make_float4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
+  };
+
+  load(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < a.K; k0 += FK) {
+    const bool more = k0 + FK < a.K;
+    if (more) load(k0 + FK);
+#pragma unroll
+    for (int kk = 0; kk < FK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][4 * ty]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][32 + 4 * ty]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][4 * tx]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][32 + 4 * tx]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  float* C = reinterpret_cast<float*>(a.C) + bz * a.sC;
+  const float* R = a.residual ? reinterpret_cast<const float*>(a.residual) + bz * a.sC : nullptr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int gm = m0 + (i < 4 ? 4 * ty + i : 32 + 4 * ty + i - 4);
+    if (gm >= a.M) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gn = n0 + h * 32 + 4 * tx;
+      if (gn >= a.N) continue;
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x = acc[i][4 * h + j];
+        if (a.epi != AFG_EPI_NONE) x = apply_act_rt(a.epi, x + a.bias[gn + j]);
+        if (R) x = x + R[static_cast<int64_t>(gm) * a.ldc + gn + j];
+        v[j] = x;
+      }
+      *reinterpret_cast<float4*>(C + static_cast<int64_t>(gm) * a.ldc + gn) =
+          make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
 template <typename TA>
 cudaError_t launch_c(afg_dtype c, const SimtArgs& a, int64_t batch, cudaStream_t s) {
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, static_cast<unsigned>(batch));
@@ -175,6 +300,23 @@ afg_status gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, con
   a.b_nk = b_layout == AFG_B_NK;
   a.epi = static_cast<int>(epi);
   cudaError_t e;
+  // the fp32 8x8-register-block kernel when every row is float4-addressable
+  const bool fast = ab == AFG_F32 && c == AFG_F32 && !a.b_nk && lda % 4 == 0 && ldb % 4 == 0 &&
+                    ldc % 4 == 0 && N % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(B) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+                    (residual == nullptr || (reinterpret_cast<uintptr_t>(residual) & 15) == 0) &&
+                    (sA % 4 == 0) && (sB % 4 == 0) && (sC % 4 == 0);
+  static const bool no_fast = [] {  // AFG_SIMT_FAST=0: the general kernel (A/B measurements)
+    const char* e = getenv("AFG_SIMT_FAST");
+    return e && atoi(e) == 0;
+  }();
+  if (fast && !no_fast) {
+    dim3 grid((a.N + FT - 1) / FT, (a.M + FT - 1) / FT, static_cast<unsigned>(batch));
+    gemm_f32_8x8_kernel<<<grid, 64, 0, stream>>>(a);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "gemm_f32_8x8 launch");
+  }
   switch (ab) {
     case AFG_F32: e = launch_c<float>(c, a, batch, stream); break;
     case AFG_F16: e = launch_c<__half>(c, a, batch, stream); break;

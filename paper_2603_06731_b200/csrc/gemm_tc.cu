@@ -777,12 +777,8 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB,
   auto kern = gemm_tc_kernel<BLOCK_N, STAGES, B_MN_MAJOR, AB_BF16, OutT, IM2COL, PAIR, NG>;
   constexpr int smem = SmemLayout<BLOCK_N, STAGES, PAIR, NG>::TOTAL;
   static_assert(smem <= 232448, "gemm smem over the 227 KB opt-in limit");
-  static bool configured = false;  // per-instantiation, per-process
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // per instantiation, one bit per device
+  if (cudaError_t e = ensure_smem_optin(configured, kern, smem); e != cudaSuccess) return e;
   const int tiles = args.num_m_blocks * args.num_n_blocks;
   // persistent grid (CTA pairs: clusters of 2 on one TPC, one per 2 SMs),
   // launched as a programmatic dependent of the previous kernel in the stream
@@ -1096,8 +1092,6 @@ afg_status conv_halo(const void* x, const void* w, const float* bias, void* y, i
   const int tiles = a.num_m_tiles * a.g.num_n_blocks;
   const int grid = std::min(tiles, num_sms());
   auto go = [&](auto kern, int smem) {
-    static bool configured = false;
-    (void)configured;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};

@@ -76,6 +76,8 @@ def conv2d_nhwc_i8(x, w_ohwi, stride=(1, 1), pad=(0, 0), dil=(1, 1), out_hw=None
     [OC,KH,KW,C]; pad = (top, left); out_hw defaults to symmetric padding.
     Returns [B,OH,OW,OC] int32 / int8 / float32 by out_mode (as gemm_i8)."""
     _need_cuda(x, w_ohwi)
+    if x.dtype != torch.int8 or w_ohwi.dtype != torch.int8:
+        raise AfgError(1, "conv2d_nhwc_i8 takes int8 operands")
     B, H, W, C = x.shape
     OC, KH, KW, _ = w_ohwi.shape
     if out_hw is None:
