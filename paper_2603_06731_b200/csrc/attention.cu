@@ -727,9 +727,9 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
   if (cudaError_t e = ensure_smem_optin(configured, kern, smem); e != cudaSuccess) return e;
   const int units = a.BH * ((a.Nq + 2 * BM - 1) / (2 * BM));
   const unsigned grid = static_cast<unsigned>(std::min(units, num_sms()));  // persistent
-  static const int sched_env = [] {  // AFG_ATTN_SCHED=0: the in-kernel snake order (A/B)
+  static const int sched_env = [] {  // AFG_ATTN_SCHED=1: the LPT table (measured slower, §7b)
     const char* e = getenv("AFG_ATTN_SCHED");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   a.sched = a.sched_off = a.sched_cnt = nullptr;
   if (sched_env) {

@@ -217,14 +217,21 @@ __global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
   for (int k0 = 0; k0 < a.K; k0 += FK) {
     const bool more = k0 + FK < a.K;
     if (more) load(k0 + FK);
+    // fragments of step kk+1 are read while step kk's 64 FMAs issue
+    float4 a0 = *reinterpret_cast<const float4*>(&As[buf][0][4 * ty]);
+    float4 a1 = *reinterpret_cast<const float4*>(&As[buf][0][32 + 4 * ty]);
+    float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][0][4 * tx]);
+    float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][0][32 + 4 * tx]);
 #pragma unroll
     for (int kk = 0; kk < FK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][4 * ty]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][32 + 4 * ty]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][4 * tx]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][32 + 4 * tx]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      if (kk + 1 < FK) {
+        a0 = *reinterpret_cast<const float4*>(&As[buf][kk + 1][4 * ty]);
+        a1 = *reinterpret_cast<const float4*>(&As[buf][kk + 1][32 + 4 * ty]);
+        b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk + 1][4 * tx]);
+        b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk + 1][32 + 4 * tx]);
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll

@@ -1701,6 +1701,11 @@ class Planner {
     const int64_t KH = wd.shape[2], KW = wd.shape[3], OC = od.shape[1];
     const Window wy = conv_window(H, KH, n.strideY, n.dilY, n.samePadding, n.transposed);
     const Window wx = conv_window(W, KW, n.strideX, n.dilX, n.samePadding, n.transposed);
+    if (is_float(xd.dtype) && xd.dtype == wd.dtype && od.dtype == ElementType::F32 &&
+        C % 64 == 0 && R_.has(n.inputs[0]) && R_.has(n.inputs[1])) {
+      const afg_dtype t = tc_type({n.inputs[0], n.inputs[1]});
+      if (t != AFG_F32) return run_conv_tc(i, wy, wx, t);
+    }
     if (is_float(xd.dtype) && xd.dtype == wd.dtype && od.dtype == ElementType::F32) {
       DevTensor& Y = R_.alloc(n.output, od.shape, ElementType::F32);
       // the direct kernel takes the interpreter's begin pads; transposed convs
@@ -1713,6 +1718,72 @@ class Planner {
       return;
     }
     run_conv_vm(i, wy, wx);
+  }
+
+  // conv2d in the reference's NCHW / OIHW (IOHW transposed) layout on the
+  // implicit-GEMM tensor-core kernel, for bf16 / f16-valued operands: the
+  // input is re-laid out NHWC in the 16-bit type (exact), the filter packed
+  // OHWI (flipped and transposed for a transposed conv), the fp32 result
+  // permuted back to NCHW. Every conv variant of frontend.cpp:752-970 maps
+  // onto the kernel's explicit geometry: stride / dilation / begin pads
+  // (the far pads follow from OH, OW); a transposed conv is a stride-1 conv
+  // over the zero-stuffed input (frontend.cpp:764-803) whose begin pad is
+  // (K-1)*dil minus the dropped half of the same-pad.
+  void run_conv_tc(int i, const Window& wy, const Window& wx, afg_dtype t) {
+    const TensorOpNode& n = op(i);
+    const TensorDesc& xd = desc(n.inputs[0]);
+    const TensorDesc& wd = desc(n.inputs[1]);
+    const TensorDesc& od = desc(n.output);
+    const int64_t B = xd.shape[0], C = xd.shape[1], H = xd.shape[2], W = xd.shape[3];
+    const int64_t KH = wd.shape[2], KW = wd.shape[3], OC = od.shape[1];
+    const ElementType et = t == AFG_BF16 ? ElementType::BF16 : ElementType::F16;
+    const int64_t sy = n.transposed ? n.strideY : 1, sx = n.transposed ? n.strideX : 1;
+    // NHWC input (zero-stuffed when transposed)
+    const int64_t IH = (H - 1) * sy + 1, IW = (W - 1) * sx + 1;
+    const std::string X = "$tcx_" + n.output, Wt = "$tcw_" + n.output, Y = "$tcy_" + n.output;
+    DevTensor& xt = R_.alloc(X, {B, IH, IW, C}, et);
+    if (n.transposed)
+      cudaMemsetAsync(xt.ptr, 0, static_cast<size_t>(xt.numel()) * 2, R_.stream());
+    {
+      NestBuilder nb(*this);
+      nb.frame(xd.shape);  // b, c, y, x
+      const std::string v = nb.load(n.inputs[0], {nb.iv(0), nb.iv(1), nb.iv(2), nb.iv(3)});
+      nb.store(X, v, {nb.iv(0), mulc(nb.iv(2), sy), mulc(nb.iv(3), sx), nb.iv(1)});
+      R_.run_vm(nb.finish(), no_priv());
+    }
+    // filter [OC, KH, KW, C] in the 16-bit type
+    R_.alloc(Wt, {OC, KH, KW, C}, et);
+    {
+      NestBuilder nb(*this);
+      nb.frame({OC, KH, KW, C});  // oc, ky, kx, c
+      std::string v;
+      if (!n.transposed) {
+        v = nb.load(n.inputs[1], {nb.iv(0), nb.iv(3), nb.iv(1), nb.iv(2)});
+      } else {  // IOHW, flipped taps
+        v = nb.load(n.inputs[1], {nb.iv(3), nb.iv(0),
+                                  add(mulc(nb.iv(1), -1), gpu::IndexExpr::constant(KH - 1)),
+                                  add(mulc(nb.iv(2), -1), gpu::IndexExpr::constant(KW - 1))});
+      }
+      nb.store(Wt, v, {nb.iv(0), nb.iv(1), nb.iv(2), nb.iv(3)});
+      R_.run_vm(nb.finish(), no_priv());
+    }
+    const int64_t pt = n.transposed ? (KH - 1) * n.dilY - wy.pad : wy.pad;
+    const int64_t pl = n.transposed ? (KW - 1) * n.dilX - wx.pad : wx.pad;
+    DevTensor& yt = R_.alloc(Y, {B, wy.out, wx.out, OC}, ElementType::F32);
+    ok(afg_conv2d_nhwc_ex(R_.at(X).ptr, R_.at(Wt).ptr, nullptr, yt.ptr, B, IH, IW, C, OC, KH, KW,
+                          n.transposed ? 1 : n.strideY, n.transposed ? 1 : n.strideX, pt, pl,
+                          n.dilY, n.dilX, wy.out, wx.out, t, AFG_F32, AFG_EPI_NONE,
+                          R_.stream()));
+    R_.alloc(n.output, od.shape, ElementType::F32);
+    run_copy_permuted(Y, n.output, {0, 3, 1, 2});
+    R_.release(X);
+    R_.release(Wt);
+    R_.release(Y);
+    plan(std::string("afg_conv2d_nhwc[conv_tc ") + (t == AFG_BF16 ? "bf16 " : "f16 ") +
+         dims_str(xd.shape) + " k" + std::to_string(KH) + "x" + std::to_string(KW) + " s" +
+         std::to_string(n.strideY) + " d" + std::to_string(n.dilY) +
+         (n.samePadding ? " same" : " valid") + (n.transposed ? " transposed" : "") +
+         "] NCHW conv2d -> " + n.output);
   }
 
   // The interpreter's conv nest (frontend.cpp:752-970 semantics) on the VM,

@@ -122,6 +122,10 @@ def cases():
                 "afg_gemm_i8"))
     g, f = conv_i8_graph(2, 32, 10, 10, 48, 3, "same")
     out.append(("conv_i8_same_32to48", 61, g, f, 0.0, 1.0, [], 0.0, "afg_conv2d_nhwc_i8"))
+    from oracle.graphs import bert_layer_graph
+    g, f, _ = bert_layer_graph(64, 128, 2, 512)
+    out.append(("bert_layer_graph_s64_h128", 62, g, f, -0.5, 0.5,
+                ["x", "wq", "wk", "wv", "wo", "w1", "w2"], 1e-4, "afg_attention_fwd"))
     return out
 
 
