@@ -149,29 +149,37 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtArgs a) {
 // LDS.128 instead of 16 per 8 LDS.32).
 constexpr int FT = 64, FK = 16;
 
-__global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
+// TX thread columns x 8 thread rows: TX = 8 -> 64 threads, 8x8 outputs each;
+// TX = 16 -> 128 threads, 8x4 each (twice the warps to hide the LDS latency).
+template <int TX>
+__global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) {
+  constexpr int T = 8 * TX;            // threads
+  constexpr int CN = 64 / TX;          // columns per thread (8 or 4)
+  constexpr int AK = FK * FT / T;      // A values each thread loads per slab
+  constexpr int BV = FK * FT / T;      // B values each thread loads per slab
   __shared__ __align__(16) float As[2][FK][FT + 4];
   __shared__ __align__(16) float Bs[2][FK][FT + 4];
   const int tid = threadIdx.x;
-  const int tx = tid % 8, ty = tid / 8;
+  const int tx = tid % TX, ty = tid / TX;
   const int m0 = blockIdx.y * FT, n0 = blockIdx.x * FT;
   const int64_t bz = blockIdx.z;
   const float* A = reinterpret_cast<const float*>(a.A) + bz * a.sA;
   const float* B = reinterpret_cast<const float*>(a.B) + bz * a.sB;
-  float acc[8][8];
+  float acc[8][CN];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < CN; ++j) acc[i][j] = 0.0f;
 
-  // loaders: thread t reads A row m0+t (16 k), and B row k0 + t/4, 16 columns
-  float ra[FK], rb[16];
-  const int bk = tid / 4, bn = (tid % 4) * 16;
+  // A: thread reads AK consecutive k of row am; B: BV consecutive columns of row bk
+  const int am = tid / (FK / AK), ak0 = (tid % (FK / AK)) * AK;
+  const int bk = tid / (FT / BV), bn = (tid % (FT / BV)) * BV;
+  float ra[AK], rb[BV];
   auto load = [&](int k0) {
-    const int gm = m0 + tid;
+    const int gm = m0 + am;
 #pragma unroll
-    for (int q = 0; q < FK / 4; ++q) {
-      const int gk = k0 + 4 * q;
+    for (int q = 0; q < AK / 4; ++q) {
+      const int gk = k0 + ak0 + 4 * q;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (gm < a.M) {
         if (gk + 3 < a.K) {
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
     }
     const int gk = k0 + bk;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < BV / 4; ++q) {
       const int gn = n0 + bn + 4 * q;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (gk < a.K && gn < a.N)  // N % 4 == 0 on this path
@@ -203,11 +211,17 @@ __global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int k = 0; k < FK; ++k) As[buf][k][tid] = ra[k];
+    for (int k = 0; k < AK; ++k) As[buf][ak0 + k][am] = ra[k];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < BV / 4; ++q)
       *reinterpret_cast<float4*>(&Bs[buf][bk][bn + 4 * q]) =
           make_float4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
+  };
+  auto frag = [&](int buf, int kk, float4& a0, float4& a1, float4& b0, float4& b1) {
+    a0 = *reinterpret_cast<const float4*>(&As[buf][kk][4 * ty]);
+    a1 = *reinterpret_cast<const float4*>(&As[buf][kk][32 + 4 * ty]);
+    b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][4 * tx]);
+    if constexpr (CN == 8) b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][32 + 4 * tx]);
   };
 
   load(0);
@@ -217,25 +231,18 @@ __global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
   for (int k0 = 0; k0 < a.K; k0 += FK) {
     const bool more = k0 + FK < a.K;
     if (more) load(k0 + FK);
-    // fragments of step kk+1 are read while step kk's 64 FMAs issue
-    float4 a0 = *reinterpret_cast<const float4*>(&As[buf][0][4 * ty]);
-    float4 a1 = *reinterpret_cast<const float4*>(&As[buf][0][32 + 4 * ty]);
-    float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][0][4 * tx]);
-    float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][0][32 + 4 * tx]);
+    // fragments of step kk+1 are read while step kk's FMAs issue
+    float4 a0, a1, b0, b1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    frag(buf, 0, a0, a1, b0, b1);
 #pragma unroll
     for (int kk = 0; kk < FK; ++kk) {
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-      if (kk + 1 < FK) {
-        a0 = *reinterpret_cast<const float4*>(&As[buf][kk + 1][4 * ty]);
-        a1 = *reinterpret_cast<const float4*>(&As[buf][kk + 1][32 + 4 * ty]);
-        b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk + 1][4 * tx]);
-        b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk + 1][32 + 4 * tx]);
-      }
+      if (kk + 1 < FK) frag(buf, kk + 1, a0, a1, b0, b1);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < CN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     if (more) {
       stash(buf ^ 1);
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(64) gemm_f32_8x8_kernel(const SimtArgs a) {
     const int gm = m0 + (i < 4 ? 4 * ty + i : 32 + 4 * ty + i - 4);
     if (gm >= a.M) continue;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < CN / 4; ++h) {
       const int gn = n0 + h * 32 + 4 * tx;
       if (gn >= a.N) continue;
       float v[4];
@@ -319,10 +326,17 @@ afg_status gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, con
     return e && atoi(e) == 0;
   }();
   if (fast && !no_fast) {
+    static const int variant = [] {  // AFG_SIMT_TPB = 64 | 128 (threads per 64x64 tile)
+      const char* e = getenv("AFG_SIMT_TPB");
+      return e ? atoi(e) : 128;
+    }();
     dim3 grid((a.N + FT - 1) / FT, (a.M + FT - 1) / FT, static_cast<unsigned>(batch));
-    gemm_f32_8x8_kernel<<<grid, 64, 0, stream>>>(a);
+    if (variant == 64)
+      gemm_f32_blk_kernel<8><<<grid, 64, 0, stream>>>(a);
+    else
+      gemm_f32_blk_kernel<16><<<grid, 128, 0, stream>>>(a);
     count_launch();
-    return cuda_status(cudaGetLastError(), "gemm_f32_8x8 launch");
+    return cuda_status(cudaGetLastError(), "gemm_f32_blk launch");
   }
   switch (ab) {
     case AFG_F32: e = launch_c<float>(c, a, batch, stream); break;

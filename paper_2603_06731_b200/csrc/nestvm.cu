@@ -26,6 +26,10 @@
 #include <set>
 #include <sstream>
 #include <stdexcept>
+#include <dlfcn.h>
+#include <mutex>
+#include <nvrtc.h>
+#include <type_traits>
 
 #include "nestvm.h"
 
@@ -49,6 +53,8 @@ constexpr int NIV = 32;
 constexpr int64_t EXPR_END = -1;
 constexpr int64_t EXPR_IV = 101;  // resolved Dim: immediate = iv slot
 constexpr size_t kErrBytes = 8 + 8 + 8 * NIV;
+// threads x instructions above which a nest is compiled instead of interpreted
+constexpr double kJitWork = 1 << 21;
 
 enum VmOp : int32_t {
   OP_LOOP = 1, OP_END, OP_LOAD, OP_STORE, OP_ARITH, OP_IVVAL, OP_MMA_LOAD, OP_MMA_COMPUTE,
@@ -754,6 +760,322 @@ cudaError_t launch_vm(const VmArgs& a, unsigned grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------- JIT -------
+// The same encoded nest, compiled: the instruction stream is translated to
+// CUDA C (loops -> for loops, loads / stores -> typed accesses with the bounds
+// check, arithmetic -> the interpreter's double operations with explicit
+// _rn intrinsics, no contraction) and compiled once per distinct nest with
+// NVRTC for sm_100a (-fmad=false), cached per device. Same semantics as the
+// interpreting kernel, at memory speed: the graph planner's fused regions and
+// the program executor's large nests run through it; small nests, counting
+// mode and fragment ops stay on the interpreter.
+
+namespace jit {
+
+struct Nvrtc {
+  bool ok = false;
+  std::string why;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*,
+                        const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      n.why = "libnvrtc.so.12 not loadable";
+      return;
+    }
+    auto sym = [&](auto& f, const char* name) {
+      f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+      return f != nullptr;
+    };
+    n.ok = sym(n.create, "nvrtcCreateProgram") && sym(n.compile, "nvrtcCompileProgram") &&
+           sym(n.cubin_size, "nvrtcGetCUBINSize") && sym(n.cubin, "nvrtcGetCUBIN") &&
+           sym(n.log_size, "nvrtcGetProgramLogSize") && sym(n.log, "nvrtcGetProgramLog") &&
+           sym(n.destroy, "nvrtcDestroyProgram");
+    if (!n.ok) n.why = "libnvrtc lacks a symbol";
+  });
+  return n;
+}
+
+constexpr int MAX_BUFS = 48;
+struct JitArgs {
+  char* ptr[MAX_BUFS];
+  int* err;
+  long long total;
+};
+
+std::string lit(double v) {
+  uint64_t u;
+  std::memcpy(&u, &v, 8);
+  char b[64];
+  std::snprintf(b, sizeof(b), "__longlong_as_double(0x%016llxLL)", static_cast<unsigned long long>(u));
+  return b;
+}
+
+const char* kPrelude = R"(
+typedef long long LL;
+__device__ __forceinline__ LL fdiv(LL a, LL b) { LL q = a / b; if ((a % b != 0) && ((a < 0) != (b < 0))) --q; return q; }
+__device__ __forceinline__ LL fmd(LL a, LL b) { LL r = a % b; if (r != 0 && ((r < 0) != (b < 0))) r += b; return r; }
+__device__ __forceinline__ float h2f(unsigned short h) { float f; asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h)); return f; }
+__device__ __forceinline__ unsigned short f2h(float f) { unsigned short h; asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
+__device__ __forceinline__ float b2f(unsigned short h) { return __uint_as_float(((unsigned)h) << 16); }
+__device__ __forceinline__ unsigned short f2b(float f) { unsigned short h; asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
+__device__ __forceinline__ double rt0(double v) { return (double)__double2float_rn(v); }
+__device__ __forceinline__ double rt1(double v) { return (double)h2f(f2h(__double2float_rn(v))); }
+__device__ __forceinline__ double rt2(double v) { return (double)b2f(f2b(__double2float_rn(v))); }
+__device__ __forceinline__ double rt3(double v) { return fmin(fmax(rint(v), -128.0), 127.0); }
+__device__ __forceinline__ double rt4(double v) { return fmin(fmax(rint(v), -2147483648.0), 2147483647.0); }
+__device__ __forceinline__ double rt5(double v) { return v; }
+struct JitArgs { char* ptr[48]; int* err; LL total; };
+)";
+
+const char* ld_expr(int t) {
+  switch (t) {
+    case VT_F32: return "(double)((const float*)%s)[%s]";
+    case VT_F16: return "(double)h2f(((const unsigned short*)%s)[%s])";
+    case VT_BF16: return "(double)b2f(((const unsigned short*)%s)[%s])";
+    case VT_I8: return "(double)((const signed char*)%s)[%s]";
+    case VT_I32: return "(double)((const int*)%s)[%s]";
+    default: return "((const double*)%s)[%s]";
+  }
+}
+std::string st_stmt(int t, const std::string& p, const std::string& off, const std::string& v) {
+  switch (t) {
+    case VT_F32: return "((float*)" + p + ")[" + off + "] = (float)(" + v + ");";
+    case VT_F16: return "((unsigned short*)" + p + ")[" + off + "] = f2h((float)(" + v + "));";
+    case VT_BF16: return "((unsigned short*)" + p + ")[" + off + "] = f2b((float)(" + v + "));";
+    case VT_I8: return "((signed char*)" + p + ")[" + off + "] = (signed char)(" + v + ");";
+    case VT_I32: return "((int*)" + p + ")[" + off + "] = (int)(" + v + ");";
+    default: return "((double*)" + p + ")[" + off + "] = " + v + ";";
+  }
+}
+
+// postfix index program -> C expression
+std::string cexpr(const std::vector<int64_t>& ex, int32_t off) {
+  std::vector<std::string> st;
+  for (size_t k = static_cast<size_t>(off);;) {
+    const int64_t op = ex[k++];
+    if (op == EXPR_END) break;
+    switch (op) {
+      case IndexExpr::Const: st.push_back("(" + std::to_string(ex[k++]) + "LL)"); break;
+      case EXPR_IV: st.push_back("i" + std::to_string(ex[k++])); break;
+      case IndexExpr::Add: {
+        const std::string b = st.back();
+        st.pop_back();
+        st.back() = "(" + st.back() + " + " + b + ")";
+        break;
+      }
+      case IndexExpr::MulConst: st.back() = "(" + st.back() + " * " + std::to_string(ex[k++]) + "LL)"; break;
+      case IndexExpr::FloorDiv: st.back() = "fdiv(" + st.back() + ", " + std::to_string(ex[k++]) + "LL)"; break;
+      case IndexExpr::Mod: st.back() = "fmd(" + st.back() + ", " + std::to_string(ex[k++]) + "LL)"; break;
+      default: throw InterpError("afg nest jit: bad index code");
+    }
+  }
+  return st.at(0);
+}
+
+// Source of the nest kernel, or "" when the program uses what the JIT does
+// not translate (fragments).
+std::string source(const Encoder& enc, const std::vector<VmBuf>& bt, const VmArgs& a) {
+  std::ostringstream o;
+  o << kPrelude;
+  o << "extern \"C\" __global__ void __launch_bounds__(128) nest_jit(JitArgs p) {\n";
+  o << "  const LL nth = (LL)gridDim.x * blockDim.x;\n";
+  o << "  const LL tid = (LL)blockIdx.x * blockDim.x + threadIdx.x;\n";
+  const int niv = static_cast<int>(enc.iv.size());
+  const int nreg = static_cast<int>(enc.reg.size());
+  for (int i = 0; i < niv; ++i) o << "  LL i" << i << " = 0;\n";
+  for (int r = 0; r < nreg; ++r) o << "  double r" << r << " = 0.0;\n";
+  for (size_t b = 0; b < bt.size(); ++b) {
+    o << "  char* P" << b << " = p.ptr[" << b << "]";
+    if (bt[b].priv) o << " + tid * " << bt[b].priv * vm_type_bytes(static_cast<VmType>(bt[b].type)) << "LL";
+    o << ";\n";
+  }
+  o << "  for (LL t = tid; t < p.total; t += nth) {\n    LL rem = t;\n";
+  uint32_t live = 0;
+  for (int l = a.npar - 1; l >= 0; --l) {
+    o << "    i" << a.par_slot[l] << " = " << a.par_lo[l] << "LL + (rem % " << a.par_ext[l]
+      << "LL) * " << a.par_step[l] << "LL; rem /= " << a.par_ext[l] << "LL;\n";
+    live |= 1u << a.par_slot[l];
+  }
+  std::vector<uint32_t> live_stack;
+  auto operand = [&](int32_t x) {
+    return x >= 0 ? "r" + std::to_string(x) : lit(enc.consts.at(-x - 1));
+  };
+  auto list = [&](int32_t at, const char* fn) {
+    const int32_t n = enc.lists.at(at);
+    std::string e = cexpr(enc.expr, enc.lists.at(at + 1));
+    for (int32_t i = 1; i < n; ++i)
+      e = std::string(fn) + "(" + e + ", " + cexpr(enc.expr, enc.lists.at(at + 1 + i)) + ")";
+    return e;
+  };
+  auto fail = [&](int code, int buf) {
+    std::ostringstream f;
+    f << "{ if (atomicCAS(p.err, 0, " << code << ") == 0) { p.err[1] = " << buf
+      << "; LL* tr = (LL*)(p.err + 2); tr[0] = " << live << "LL;";
+    for (int i = 0; i < niv; ++i) f << " tr[" << 1 + i << "] = i" << i << ";";
+    f << " } return; }";
+    return f.str();
+  };
+  auto address = [&](int32_t list_at, int b, int64_t row_extra = 0, int64_t col_extra = 0) {
+    const VmBuf& vb = bt.at(b);
+    const int32_t n = enc.lists.at(list_at);
+    std::ostringstream s2;
+    if (n != vb.rank) {
+      s2 << fail(2, b);
+      return std::make_pair(s2.str(), std::string("0"));
+    }
+    std::string off = "0LL";
+    for (int d = 0; d < n; ++d) {
+      std::string x = cexpr(enc.expr, enc.lists.at(list_at + 1 + d));
+      (void)row_extra;
+      (void)col_extra;
+      s2 << "const LL x" << d << " = " << x << "; if (x" << d << " < 0 || x" << d << " >= "
+         << vb.shape[d] << "LL) " << fail(1, b) << "\n";
+      off = off + " + x" + std::to_string(d) + " * " + std::to_string(vb.stride[d]) + "LL";
+    }
+    return std::make_pair(s2.str(), off);
+  };
+  for (size_t pc = 0; pc < enc.code.size(); ++pc) {
+    const Ins& in = enc.code[pc];
+    switch (in.op) {
+      case OP_LOOP:
+        o << "    { const LL lb" << pc << " = " << list(in.b, "max") << "; const LL ub" << pc
+          << " = " << list(in.c, "min") << ";\n    for (i" << in.a << " = lb" << pc << "; i" << in.a
+          << " < ub" << pc << "; i" << in.a << " += " << in.d << "LL) {\n";
+        live_stack.push_back(live);
+        live |= 1u << in.a;
+        break;
+      case OP_END:
+        o << "    } }\n";
+        live = live_stack.back();
+        live_stack.pop_back();
+        break;
+      case OP_IVVAL: o << "    r" << in.a << " = (double)i" << in.b << ";\n"; break;
+      case OP_LOAD: {
+        const auto [chk, off] = address(in.c, in.b);
+        char buf[512];
+        std::snprintf(buf, sizeof(buf), ld_expr(bt[in.b].type), ("P" + std::to_string(in.b)).c_str(),
+                      "o_");
+        o << "    { " << chk << " const LL o_ = " << off << "; r" << in.a << " = " << buf << "; }\n";
+        break;
+      }
+      case OP_STORE: {
+        const auto [chk, off] = address(in.c, in.b);
+        const std::string v = "rt" + std::to_string(bt[in.b].type) + "(" + operand(in.a) + ")";
+        o << "    { " << chk << " const LL o_ = " << off << "; "
+          << st_stmt(bt[in.b].type, "P" + std::to_string(in.b), "o_", v) << " }\n";
+        break;
+      }
+      case OP_ARITH: {
+        const int kind = in.b & 0xff, cast = (in.b >> 8) & 0xff;
+        const std::string x = in.c != INT32_MIN ? operand(in.c) : "0.0";
+        const std::string y = in.d != INT32_MIN ? operand(in.d) : "0.0";
+        const std::string z = in.e != INT32_MIN ? operand(in.e) : "0.0";
+        std::string v;
+        switch (static_cast<ArithOp>(kind)) {
+          case ArithOp::Add: v = "__dadd_rn(" + x + ", " + y + ")"; break;
+          case ArithOp::Mul: v = "__dmul_rn(" + x + ", " + y + ")"; break;
+          case ArithOp::Sub: v = "__dsub_rn(" + x + ", " + y + ")"; break;
+          case ArithOp::Div: v = "__ddiv_rn(" + x + ", " + y + ")"; break;
+          case ArithOp::Max: v = "((" + x + ") < (" + y + ") ? (" + y + ") : (" + x + "))"; break;
+          case ArithOp::Exp: v = "exp(" + x + ")"; break;
+          case ArithOp::Negate: v = "(-(" + x + "))"; break;
+          case ArithOp::Cast:
+            v = (cast == VT_I8 || cast == VT_I32)
+                    ? "rt" + std::to_string(cast) + "(trunc(" + x + "))"
+                    : "rt" + std::to_string(cast) + "(" + x + ")";
+            break;
+          case ArithOp::Fma: v = "__dadd_rn(__dmul_rn(" + x + ", " + y + "), " + z + ")"; break;
+          case ArithOp::Select: v = "((" + x + ") != 0.0 ? (" + y + ") : (" + z + "))"; break;
+          case ArithOp::CmpEq: v = "((" + x + ") == (" + y + ") ? 1.0 : 0.0)"; break;
+          case ArithOp::CmpLt: v = "((" + x + ") < (" + y + ") ? 1.0 : 0.0)"; break;
+          case ArithOp::CmpLe: v = "((" + x + ") <= (" + y + ") ? 1.0 : 0.0)"; break;
+          case ArithOp::Quant:
+            v = "fmin(fmax(round(__ddiv_rn(" + x + ", " + lit(in.imm) + ")), -128.0), 127.0)";
+            break;
+          case ArithOp::Dequant: v = "__dmul_rn(" + x + ", " + lit(in.imm) + ")"; break;
+          case ArithOp::Round: v = "rt" + std::to_string(cast) + "(" + x + ")"; break;
+        }
+        o << "    r" << in.a << " = " << v << ";\n";
+        break;
+      }
+      default: return "";  // fragment ops: interpreter only
+    }
+  }
+  o << "  }\n}\n";
+  return o.str();
+}
+
+struct Compiled {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+};
+
+// compile-once cache per (device, source)
+cudaKernel_t get(const std::string& src) {
+  static std::mutex mu;
+  static std::map<std::pair<int, std::string>, Compiled> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, src);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second.kern;
+  const Nvrtc& n = nvrtc();
+  if (!n.ok) return nullptr;
+  nvrtcProgram prog;
+  if (n.create(&prog, src.c_str(), "afg_nest.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return nullptr;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17"};
+  const nvrtcResult r = n.compile(prog, 3, opts);
+  Compiled c;
+  if (r == NVRTC_SUCCESS) {
+    size_t sz = 0;
+    n.cubin_size(prog, &sz);
+    std::vector<char> bin(sz);
+    n.cubin(prog, bin.data());
+    if (cudaLibraryLoadData(&c.lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) ==
+            cudaSuccess &&
+        cudaLibraryGetKernel(&c.kern, c.lib, "nest_jit") == cudaSuccess) {
+      // compiled
+    } else {
+      cudaGetLastError();
+      c.kern = nullptr;
+    }
+  } else {
+    size_t ls = 0;
+    n.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    n.log(prog, log.data());
+    std::fprintf(stderr, "afg nest jit: NVRTC failed (falling back to the interpreter):\n%s\n",
+                 log.c_str());
+  }
+  n.destroy(&prog);
+  cache[key] = c;
+  return c.kern;
+}
+
+bool enabled() {
+  static const bool on = [] {
+    const char* e = getenv("AFG_NEST_JIT");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+}  // namespace jit
 }  // namespace
 
 VmType vm_type(ElementType t) {
@@ -1117,14 +1439,41 @@ std::string Runner::run_vm(const NestOp& top, const std::map<std::string, int>& 
   a.counters = counters_;
   a.err = err_;
   const size_t nregs = enc.reg.size() + 1, nfrag = enc.frag.size();
+  bool jitted = false;
+  // big nests are compiled (NVRTC, cached): same semantics, no interpretation
+  if (!counters_ && nfrag == 0 && bt.size() <= static_cast<size_t>(jit::MAX_BUFS) &&
+      static_cast<double>(a.total) * static_cast<double>(enc.code.size()) >= kJitWork &&
+      jit::enabled()) {
+    const std::string src = jit::source(enc, bt, a);
+    cudaKernel_t k = src.empty() ? nullptr : jit::get(src);
+    if (k) {
+      jit::JitArgs ja{};
+      for (size_t i = 0; i < bt.size(); ++i) ja.ptr[i] = bt[i].ptr;
+      ja.err = err_;
+      ja.total = a.total;
+      void* args[] = {&ja};
+      e = cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(128), args, 0, s_);
+      count_launch();
+      if (e != cudaSuccess) throw InterpError(std::string("afg nest jit launch: ") + cudaGetErrorString(e));
+      jitted = true;
+      plan << " jit";
+    }
+  }
   if (nfrag > 4) throw InterpError("afg nest vm: more than 4 live fragments");
   if (nfrag > 0 && nregs > 128) throw InterpError("afg nest vm: too many values with fragments");
-  if (nfrag > 0) e = launch_vm<128, 4>(a, grid, s_);
-  else if (nregs <= 32) e = launch_vm<32, 0>(a, grid, s_);
-  else if (nregs <= 128) e = launch_vm<128, 0>(a, grid, s_);
-  else if (nregs <= 512) e = launch_vm<512, 0>(a, grid, s_);
-  else throw InterpError("afg nest vm: more than 512 live values in one nest");
-  count_launch();
+  if (jitted) {
+  } else if (nfrag > 0) {
+    e = launch_vm<128, 4>(a, grid, s_);
+  } else if (nregs <= 32) {
+    e = launch_vm<32, 0>(a, grid, s_);
+  } else if (nregs <= 128) {
+    e = launch_vm<128, 0>(a, grid, s_);
+  } else if (nregs <= 512) {
+    e = launch_vm<512, 0>(a, grid, s_);
+  } else {
+    throw InterpError("afg nest vm: more than 512 live values in one nest");
+  }
+  if (!jitted) count_launch();
   if (e != cudaSuccess) throw InterpError(std::string("afg nest vm launch: ") + cudaGetErrorString(e));
   std::vector<int> herr(kErrBytes / 4, 0);
   e = cudaMemcpyAsync(herr.data(), err_, kErrBytes, cudaMemcpyDeviceToHost, s_);
