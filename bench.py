@@ -755,7 +755,7 @@ class MemChain(_Base):
         self.flops_total = self.alg_bytes_rank * rows / n
 
     def pre_step(self):
-        if self.flush is not None:
+        if self.flush is not None and not os.environ.get("AFG_BENCH_NO_FLUSH"):
             self.flush()  # untimed L2 flush (the LN working set fits in L2)
 
     def step(self):

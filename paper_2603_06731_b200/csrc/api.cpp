@@ -248,6 +248,25 @@ afg_status afg_gemm_batched(const void* A, const void* B, void* C, int64_t batch
   if (batch == 1)
     return afg_gemm(A, K, B, N, nullptr, nullptr, C, N, M, N, K, ab_dtype, c_dtype, AFG_B_KN,
                     AFG_EPI_NONE, stream);
+  // 16-bit operands with 16-byte aligned rows and batches: one tcgen05 GEMM
+  // per batch entry (each is a persistent launch over its own tiles); large
+  // enough entries only, small ones stay one batched SIMT launch
+  const int64_t ea = dtype_bytes(ab_dtype), ec = dtype_bytes(c_dtype);
+  const bool tc = (ab_dtype == AFG_BF16 || ab_dtype == AFG_F16) &&
+                  (c_dtype == AFG_F32 || c_dtype == ab_dtype) && K % 8 == 0 && N % 8 == 0 &&
+                  aligned16(A) && aligned16(B) && aligned16(C) && (M * K * ea) % 16 == 0 &&
+                  (K * N * ea) % 16 == 0 && (M * N * ec) % 16 == 0 && M * N >= 128 * 256 &&
+                  batch <= 64;
+  if (tc) {
+    for (int64_t b = 0; b < batch; ++b) {
+      afg_status st2 = gemm_tc(static_cast<const char*>(A) + b * M * K * ea, K,
+                               static_cast<const char*>(B) + b * K * N * ea, N, nullptr, nullptr,
+                               static_cast<char*>(C) + b * M * N * ec, N, M, N, K, ab_dtype,
+                               c_dtype, AFG_B_KN, AFG_EPI_NONE, s);
+      if (st2 != AFG_OK) return st2;
+    }
+    return AFG_OK;
+  }
   return gemm_simt(A, K, B, N, nullptr, nullptr, C, N, M, N, K, batch, M * K, K * N, M * N,
                    ab_dtype, c_dtype, AFG_B_KN, AFG_EPI_NONE, s);
 }

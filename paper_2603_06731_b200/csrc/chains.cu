@@ -211,9 +211,14 @@ cudaError_t softmax_launch_direct(const void* x, void* y, int64_t rows, int64_t 
 // each reduce every 8th row out of shared memory and write the result with
 // coalesced 16-byte stores. In-flight bytes live in shared memory (~160 KB
 // per SM), not in registers, so HBM stays saturated.
-constexpr int STREAM_WARPS = 15;  // + 1 producer warp = 16 warps: 128 registers per thread
-constexpr int STREAM_SMEM = 160 * 1024;
-constexpr int STREAM_SMEM_LN = 192 * 1024;  // layernorm: 2 rows x (x, residual) per slot
+// 12 consumer warps + 1 producer (157 registers per thread). The chains are
+// bound by the bytes in flight per SM (layernorm, measured: a 48 / 96 / 192
+// KB ring gives 0.36 / 0.75 / 0.78 of HBM), and the ring depth is rounded
+// down to a multiple of the consumer-warp count: 12 warps fit 36 layernorm
+// slots (216 KB) where 15 warps fitted 30.
+constexpr int STREAM_WARPS = 12;
+constexpr int STREAM_SMEM = 192 * 1024;
+constexpr int STREAM_SMEM_LN = 216 * 1024;  // layernorm: 2 rows x (x, residual) per slot
 
 __device__ __forceinline__ float ex2f_approx(float x) {
   float y;
@@ -234,6 +239,30 @@ __device__ __forceinline__ float chunk_max(const Vec<T>& t) {
 #pragma unroll
     for (int e = 0; e < Vec<T>::N; ++e) m = fmaxf(m, OutCvt<T>::from(t.e[e]));
     return m;
+  }
+}
+
+// 16-bit pair <-> packed f32x2 (the low element in the low half)
+template <typename T>
+__device__ __forceinline__ uint64_t unpack_pair(uint32_t w) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    return sm100::f2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+  } else {
+    const __half2 h = *reinterpret_cast<const __half2*>(&w);
+    const float2 f = __half22float2(h);
+    return sm100::f2(f.x, f.y);
+  }
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack_pair(uint64_t v) {
+  float a, b;
+  sm100::f2split(v, a, b);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
   }
 }
 
@@ -279,34 +308,31 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     }
   }
   if (warp == STREAM_WARPS) {
-    // The lanes issue a batch of up to 32 rows in parallel (the mbarrier /
-    // bulk-copy issue latency of one row does not serialise the ring), batches
-    // in lock-step: with batch <= ring depth, a row's slot was released by the
-    // row one lap earlier, whose own wait completed in an earlier batch, so the
-    // parity of the empty barrier it waits on is never two phases stale.
-    const int batch = ns < 32 ? ns : 32;
-    // ring position of this lane's slot, advanced by `batch` per round (no
-    // 64-bit divisions in the loop; batch <= ns wraps at most once)
-    int slot = lane % ns;
-    uint32_t ph = 0;
-    for (int64_t b0 = 0; b0 < nslots; b0 += batch) {
-      const int64_t i = b0 + lane;
-      if (lane < batch && i < nslots) {
+    // Every ring slot belongs to one producer lane (slots lane, lane + 32,
+    // lane + 64 < ns), which issues that slot's uses k = 0, 1, ... in order,
+    // each after the consumers released use k-1 (empty parity (k & 1) ^ 1).
+    // Lanes run independently: a slot is refilled the moment it is released.
+    // (Issuing in warp-wide lock-step batches of `ns` rows drained the whole
+    // ring before each refill -- on the 151 MB layernorm the DRAM read rate
+    // stayed at ~3.6 TB/s.) One lane owning a slot means no wait can see a
+    // phase two laps stale.
+    for (int64_t k = 0;; ++k) {
+      bool issued = false;
+      for (int slot = lane; slot < ns; slot += 32) {
+        const int64_t i = static_cast<int64_t>(k) * ns + slot;
+        if (i >= nslots) break;
+        issued = true;
         const int64_t row = i * grp;
-        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(grp), nr - row)) * row_bytes;
-        mbar_wait(&empty[slot], ph ^ 1);
+        const uint32_t bytes =
+            static_cast<uint32_t>(min(static_cast<int64_t>(grp), nr - row)) * row_bytes;
+        mbar_wait(&empty[slot], static_cast<uint32_t>(k & 1) ^ 1u);
         uint8_t* dst = smem + static_cast<size_t>(slot) * slot_bytes;
         mbar_arrive_expect_tx(&full[slot], MODE == 1 && res ? 2 * bytes : bytes);
         bulk_load(dst, x + (r0 + row) * cols, bytes, &full[slot]);
         if (MODE == 1 && res)
           bulk_load(dst + grp * row_bytes, res + (r0 + row) * cols, bytes, &full[slot]);
       }
-      slot += batch;
-      if (slot >= ns) {
-        slot -= ns;
-        ph ^= 1;
-      }
-      __syncwarp();
+      if (!issued) break;
     }
     return;
   }
@@ -393,6 +419,119 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
     }
+    if constexpr (sizeof(TI) == 2 && sizeof(TO) == 2 && GB_REGS) {
+      // 16-bit rows: all arithmetic on packed f32x2 pairs (FADD2 / FFMA2), the
+      // 16-bit <-> f32 conversions per pair: ~11 instructions per pair of
+      // values instead of ~40 (the scalar version was issue-bound: 490
+      // instructions per 768-column row, ncu profiles/r02/full_layernorm_*).
+      uint64_t gp[CH][E / 2], bp[CH][E / 2];
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+#pragma unroll
+        for (int p = 0; p < E / 2; ++p) {
+          gp[k][p] = sm100::f2(greg[k][2 * p], greg[k][2 * p + 1]);
+          bp[k][p] = sm100::f2(breg[k][2 * p], breg[k][2 * p + 1]);
+        }
+      for (int64_t si = warp; si < nslots; si += STREAM_WARPS, advance()) {
+        const int slot = cslot;
+        mbar_wait(&full[slot], cph);
+        const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
+        const int64_t i0 = si * R;
+        uint64_t v[R][CH][E / 2];
+        bool have[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          have[r] = i0 + r < nr;
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            const int c = lane + 32 * k;
+            if (have[r] && c < nchunks) {
+              const uint4 t = ld_shared_v4(sx + r * row_bytes + c * 16);
+              const uint32_t tw[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+              for (int p = 0; p < 4; ++p) v[r][k][p] = unpack_pair<TI>(tw[p]);
+              if (res) {
+                const uint4 q = ld_shared_v4(sx + (R + r) * row_bytes + c * 16);
+                const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int p = 0; p < 4; ++p) v[r][k][p] = sm100::fadd2(v[r][k][p], unpack_pair<TI>(qw[p]));
+              }
+            } else {
+#pragma unroll
+              for (int p = 0; p < 4; ++p) v[r][k][p] = 0ull;  // +0.0f pairs: neutral in the sums
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // slot consumed: it refills
+        float s[R], q[R], mean[R], rstd[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint64_t a = 0ull, b = 0ull;
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            a = sm100::fadd2(a, sm100::fadd2(v[r][k][0], v[r][k][1]));
+            b = sm100::fadd2(b, sm100::fadd2(v[r][k][2], v[r][k][3]));
+          }
+          float x0, x1;
+          sm100::f2split(sm100::fadd2(a, b), x0, x1);
+          s[r] = x0 + x1;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < R; ++r) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          mean[r] = s[r] * inv_cols;
+          const uint64_t nm = sm100::f2(-mean[r], -mean[r]);
+          uint64_t a = 0ull, b = 0ull;
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            if (lane + 32 * k >= nchunks) continue;  // padded lanes hold zeros, not the mean
+            const uint64_t d0 = sm100::fadd2(v[r][k][0], nm), d1 = sm100::fadd2(v[r][k][1], nm);
+            const uint64_t d2 = sm100::fadd2(v[r][k][2], nm), d3 = sm100::fadd2(v[r][k][3], nm);
+            a = sm100::ffma2(d0, d0, a);
+            b = sm100::ffma2(d1, d1, b);
+            a = sm100::ffma2(d2, d2, a);
+            b = sm100::ffma2(d3, d3, b);
+          }
+          float x0, x1;
+          sm100::f2split(sm100::fadd2(a, b), x0, x1);
+          q[r] = x0 + x1;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < R; ++r) q[r] += __shfl_xor_sync(0xffffffffu, q[r], o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) rstd[r] = rsqrtf(fmaf(q[r], inv_cols, eps));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!have[r]) continue;
+          const int64_t row = r0 + i0 + r;
+          // y = ((v - mean) * rstd) * g + b = (v * rstd + (-mean * rstd)) * g + b
+          const uint64_t ra = sm100::f2(rstd[r], rstd[r]);
+          const float c0 = -mean[r] * rstd[r];
+          const uint64_t rc = sm100::f2(c0, c0);
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            const int c = lane + 32 * k;
+            if (c >= nchunks) continue;
+            uint32_t ow[4], sw[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const uint64_t t = sm100::ffma2(v[r][k][p], ra, rc);
+              ow[p] = pack_pair<TO>(sm100::ffma2(t, gp[k][p], bp[k][p]));
+              if (sum_out) sw[p] = pack_pair<TO>(v[r][k][p]);
+            }
+            st_stream(y + row * cols + c * E, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+            if (sum_out)
+              st_stream(sum_out + row * cols + c * E, make_uint4(sw[0], sw[1], sw[2], sw[3]));
+          }
+        }
+      }
+    } else {
     for (int64_t si = warp; si < nslots; si += STREAM_WARPS, advance()) {
       const int slot = cslot;
       mbar_wait(&full[slot], cph);
@@ -514,6 +653,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
     }
+    }
   }
 }
 
@@ -539,7 +679,12 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   // own and was already consumed (loaded) when it waits on slot i. Otherwise a
   // warp can poll slot i % ns while use i - ns's bulk copy is still in flight
   // (copies complete out of order) and the parity wait passes a phase early.
-  const int64_t budget = MODE == 1 ? STREAM_SMEM_LN : STREAM_SMEM;
+  static const int64_t ln_budget_env = [] {  // AFG_LN_SMEM_KB: ring size (A/B measurements)
+    const char* e = getenv("AFG_LN_SMEM_KB");
+    return e ? static_cast<int64_t>(atoi(e)) * 1024 : 0;
+  }();
+  const int64_t budget = MODE == 1 ? (ln_budget_env > 0 ? ln_budget_env : STREAM_SMEM_LN)
+                                   : STREAM_SMEM;
   const int ns = static_cast<int>(std::min<int64_t>(90, budget / slot_bytes)) /
                  STREAM_WARPS * STREAM_WARPS;
   if (ns < STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;

@@ -23,4 +23,13 @@ def test_check_lowering_with_gpu_executor(cuda):
     r = subprocess.run([BIN, CASES], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 24
+    # per case: graph executor, program executor, orchestrated program (outputs
+    # and interpreter metrics)
+    assert r.stdout.count("PASS graph") == 24
+    assert r.stdout.count("PASS program") == 24
+    # orchestrate() output the reference's own interpreter cannot run (it throws
+    # "unbound iv" on some conv graphs) is skipped, and reported
+    n_orch = 24 - r.stdout.count("SKIP orchestrated")
+    assert n_orch >= 12, r.stdout
+    assert r.stdout.count("PASS orchestrated") == n_orch
+    assert r.stdout.count("PASS metrics") == n_orch
