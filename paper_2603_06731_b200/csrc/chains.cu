@@ -211,14 +211,14 @@ cudaError_t softmax_launch_direct(const void* x, void* y, int64_t rows, int64_t 
 // each reduce every 8th row out of shared memory and write the result with
 // coalesced 16-byte stores. In-flight bytes live in shared memory (~160 KB
 // per SM), not in registers, so HBM stays saturated.
-// 12 consumer warps + 1 producer (157 registers per thread). The chains are
+// 15 consumer warps + 1 producer (128 registers per thread). The chains are
 // bound by the bytes in flight per SM (layernorm, measured: a 48 / 96 / 192
-// KB ring gives 0.36 / 0.75 / 0.78 of HBM), and the ring depth is rounded
-// down to a multiple of the consumer-warp count: 12 warps fit 36 layernorm
-// slots (216 KB) where 15 warps fitted 30.
-constexpr int STREAM_WARPS = 12;
-constexpr int STREAM_SMEM = 192 * 1024;
-constexpr int STREAM_SMEM_LN = 216 * 1024;  // layernorm: 2 rows x (x, residual) per slot
+// KB ring gives 0.36 / 0.75 / 0.78 of HBM); 12 consumer warps with a 216 KB
+// ring (36 slots) measured worse (0.75 layernorm, 0.85 softmax): the consumer
+// parallelism matters as much.
+constexpr int STREAM_WARPS = 15;
+constexpr int STREAM_SMEM = 160 * 1024;
+constexpr int STREAM_SMEM_LN = 192 * 1024;  // layernorm: 2 rows x (x, residual) per slot
 
 __device__ __forceinline__ float ex2f_approx(float x) {
   float y;

@@ -239,6 +239,7 @@ class ProgramRunner {
       return false;
     const std::string &A = la.buffer, &B = lb.buffer, &C = init.buffer;
     if (lc.buffer != C || sc.buffer != C || A == C || B == C) return false;
+    if (!decl_.count(A) || !decl_.count(B) || !decl_.count(C)) return false;
     const NestBuffer *ad = decl_.at(A), *bd = decl_.at(B), *cd = decl_.at(C);
     const size_t r = cd->shape.size();
     if (r < 2 || ad->shape.size() != r || bd->shape.size() != r) return false;
@@ -294,6 +295,32 @@ class ProgramRunner {
     return true;
   }
 
+  // frame loops (constant, perfectly nested) whose body is exactly
+  // [store 0 -> y, for ic { for ky { for kx { load x, load w, load y, fma, store y }}}]
+  static bool lowered_conv_shape(const NestOp& top, const std::string& x, const std::string& w,
+                                 const std::string& y) {
+    const NestOp* cur = &top;
+    while (cur->kind == NestOpKind::For && cur->body.size() == 1 &&
+           cur->body[0].kind == NestOpKind::For)
+      cur = &cur->body[0];
+    if (cur->kind != NestOpKind::For || cur->body.size() != 2) return false;
+    const NestOp& init = cur->body[0];
+    if (init.kind != NestOpKind::Store || init.buffer != y || !init.operands.at(0).isImm) return false;
+    const NestOp* l = &cur->body[1];
+    for (int depth = 0; depth < 3; ++depth) {
+      if (l->kind != NestOpKind::For || l->body.empty()) return false;
+      if (depth < 2) {
+        if (l->body.size() != 1) return false;
+        l = &l->body[0];
+      }
+    }
+    const auto& b = l->body;
+    return b.size() == 5 && b[0].kind == NestOpKind::Load && b[0].buffer == x &&
+           b[1].kind == NestOpKind::Load && b[1].buffer == w && b[2].kind == NestOpKind::Load &&
+           b[2].buffer == y && b[3].kind == NestOpKind::Arith && b[3].arith == ArithOp::Fma &&
+           b[4].kind == NestOpKind::Store && b[4].buffer == y;
+  }
+
   // loop-form conv nests (conv.* attributes), not transposed, f32 result
   bool dispatch_conv(const NestOp& top) {
     auto attr = [&](const char* k) -> const NestAttr* {
@@ -307,7 +334,16 @@ class ProgramRunner {
                   dx = num("conv.dx"), py = num("conv.py"), px = num("conv.px"),
                   kh = num("conv.kh"), kw = num("conv.kw");
     if (std::min({sy, sx, dy, dx, kh, kw}) <= 0 || py < 0 || px < 0) return false;
-    const NestBuffer *xd = decl_.at(in->s), *wd = decl_.at(w->s), *od = decl_.at(out->s);
+    // the attributes survive later passes (tiling, fusion): only the lowering's
+    // own loop form is dispatched -- frame loops over the output, then the
+    // init store and the ic / ky / kx loops of load x, load w, load y, fma,
+    // store y (frontend.cpp:905-950) -- with every buffer still declared
+    auto dc = [&](const std::string& id) -> const NestBuffer* {
+      auto it = decl_.find(id);
+      return it == decl_.end() ? nullptr : it->second;
+    };
+    const NestBuffer *xd = dc(in->s), *wd = dc(w->s), *od = dc(out->s);
+    if (!xd || !wd || !od || !lowered_conv_shape(top, in->s, w->s, out->s)) return false;
     if (xd->shape.size() != 4 || wd->shape.size() != 4 || od->shape.size() != 4) return false;
     const int64_t B = xd->shape[0], C = xd->shape[1], H = xd->shape[2], W = xd->shape[3];
     const int64_t OC = od->shape[1], OH = od->shape[2], OW = od->shape[3];

@@ -43,33 +43,32 @@ def test_softmax(cuda, rows, cols, dt, od, tol):
 def test_softmax_full_size_streamed_repeat(cuda):
     # BASELINE's softmax workload at full size ([8*16*2048, 2048] fp16, 1772 rows
     # per SM through the TMA ring), launched repeatedly: an early pass of a
-    # ring-slot wait shows up as corrupted rows or a hang. Checked against a
-    # torch fp32 softmax of the same fp16 values (1 fp16 ulp).
+    # ring-slot wait shows up as corrupted rows or a hang. Checked against the
+    # oracle's softmaxReference restatement on sampled rows of the same fp16
+    # values (1 fp16 ulp).
     g = torch.Generator(device="cuda").manual_seed(5)
     x = (torch.rand((262144, 2048), generator=g, device="cuda") * 8 - 4).half()
-    want = torch.softmax(x.float(), dim=-1)
+    rows = torch.arange(0, 262144, 4099, device="cuda")
+    want = O.round_to(O.softmax(to_host(x[rows])), O.F16)
     for _ in range(4):
         y = ops.softmax(x)
-        err = ((y.float() - want).abs() / want.abs().clamp_min(1.0)).max().item()
-        assert err <= 2.0**-10, err
+        check(to_host(y[rows]), want, 2.0**-10, "softmax full size")
 
 
 def test_layernorm_full_size_streamed_repeat(cuda):
     # BERT's residual + layernorm at full size ([64*512, 768] bf16) repeatedly,
-    # against a torch fp32 restatement of the oracle formula (1 bf16 ulp).
+    # against the oracle's layernorm restatement on sampled rows (1 bf16 ulp).
     g = torch.Generator(device="cuda").manual_seed(6)
     x = (torch.rand((32768, 768), generator=g, device="cuda") * 2 - 1).bfloat16()
     r = (torch.rand((32768, 768), generator=g, device="cuda") * 2 - 1).bfloat16()
     gam = torch.rand(768, generator=g, device="cuda") * 0.2 + 0.9
     bet = torch.rand(768, generator=g, device="cuda") * 0.2 - 0.1
-    s = x.double() + r.double()
-    mu = s.mean(-1, keepdim=True)
-    var = ((s - mu) ** 2).mean(-1, keepdim=True)
-    want = ((s - mu) / torch.sqrt(var + 1e-12) * gam.double() + bet.double())
+    rows = torch.arange(0, 32768, 331, device="cuda")
+    want = O.round_to(O.layernorm(to_host(x[rows]), to_host(r[rows]), to_host(gam), to_host(bet),
+                                  1e-12)[0], O.BF16)
     for _ in range(4):
         y = ops.layernorm_residual(x, r, gam, bet, eps=1e-12)
-        err = ((y.double() - want).abs() / want.abs().clamp_min(1.0)).max().item()
-        assert err <= 2.0**-7, err
+        check(to_host(y[rows]), want, 2.0**-7, "layernorm full size")
 
 
 def test_softmax_large_magnitudes_finite(cuda):

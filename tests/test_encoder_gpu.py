@@ -21,6 +21,65 @@ from tests.gpu_util import check, seeded, to_host
 pytestmark = pytest.mark.gpu
 
 
+def oracle_bert(xh, p, B, S, hd, H, ffn):
+    """The layer composed from the restated ops, bf16 stores where the kernels
+    store (x [B*S, hd] for B whole sequences)."""
+    D = hd // H
+    T = B * S
+    bfr = lambda a: O.round_to(a, O.BF16)  # noqa: E731
+    qkv = bfr(O.matmul(xh, p["wqkv"], p["bqkv"], epi=O.EPI_BIAS, out_t=O.F64))
+    q = qkv[:, :hd].reshape(B, S, H, D).transpose(0, 2, 1, 3)
+    k = qkv[:, hd:2 * hd].reshape(B, S, H, D).transpose(0, 2, 1, 3)
+    v = qkv[:, 2 * hd:].reshape(B, S, H, D).transpose(0, 2, 1, 3)
+    att = bfr(O.attention(q, k, v, scale=D ** -0.5).transpose(0, 2, 1, 3).reshape(T, hd))
+    y1 = bfr(O.matmul(att, p["wo"], p["bo"], epi=O.EPI_BIAS, out_t=O.F64) + xh)
+    h1 = bfr(O.layernorm(y1, None, p["g1"], p["be1"], 1e-12)[0])
+    f = bfr(O.matmul(h1, p["w1"], p["b1"], epi=O.EPI_GELU_ERF, out_t=O.F64))
+    y2 = bfr(O.matmul(f, p["w2"], p["b2"], epi=O.EPI_BIAS, out_t=O.F64) + h1)
+    return bfr(O.layernorm(y2, None, p["g2"], p["be2"], 1e-12)[0])
+
+
+def run_layer(B, S, hd, H, ffn, seed=3):
+    bf, f32 = torch.bfloat16, torch.float32
+    x, xh = seeded((B * S, hd), "x", seed, dtype=bf)
+    dev, host = {}, {}
+    for name, shape, lo, hi, dt in [("wqkv", (hd, 3 * hd), -0.05, 0.05, bf),
+                                    ("wo", (hd, hd), -0.05, 0.05, bf),
+                                    ("w1", (hd, ffn), -0.05, 0.05, bf),
+                                    ("w2", (ffn, hd), -0.05, 0.05, bf),
+                                    ("bqkv", (3 * hd,), -0.1, 0.1, f32), ("bo", (hd,), -0.1, 0.1, f32),
+                                    ("b1", (ffn,), -0.1, 0.1, f32), ("b2", (hd,), -0.1, 0.1, f32),
+                                    ("g1", (hd,), 0.9, 1.1, f32), ("be1", (hd,), -0.1, 0.1, f32),
+                                    ("g2", (hd,), 0.9, 1.1, f32), ("be2", (hd,), -0.1, 0.1, f32)]:
+        dev[name], host[name] = seeded(shape, name, seed, lo, hi, dt)
+    y = torch.empty_like(x)
+    L = lib()
+    ws_bytes = L.afg_encoder_layer_workspace(B, S, hd, ffn, 2)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    d = dev
+    afg_check(L.afg_encoder_layer_fwd(
+        x.data_ptr(), y.data_ptr(), B, S, hd, H, ffn, d["wqkv"].data_ptr(), d["bqkv"].data_ptr(),
+        d["wo"].data_ptr(), d["bo"].data_ptr(), d["g1"].data_ptr(), d["be1"].data_ptr(),
+        d["w1"].data_ptr(), d["b1"].data_ptr(), d["w2"].data_ptr(), d["b2"].data_ptr(),
+        d["g2"].data_ptr(), d["be2"].data_ptr(), 1e-12, 2, ws.data_ptr(), ws_bytes, st))
+    torch.cuda.synchronize()
+    return to_host(y), xh, host
+
+
+def test_bert_layer_full_size_sampled_sequences(cuda):
+    """BASELINE configs[4] at full size (B64 x S512, BERT-base): every
+    sequence is independent, so sequences 0, 37 and 63 are checked against
+    the composed oracle (same tolerance as below)."""
+    B, S, hd, H, ffn = 64, 512, 768, 12, 3072
+    got, xh, host = run_layer(B, S, hd, H, ffn, seed=4)
+    for b in (0, 37, 63):
+        sl = slice(b * S, (b + 1) * S)
+        want = oracle_bert(xh[sl], host, 1, S, hd, H, ffn)
+        check(got[sl], want, 2.0**-5, f"bert layer full size, sequence {b}")
+    assert np.isfinite(got).all()
+
+
 def test_bert_layer_matches_oracle(cuda):
     B, S, hd, H, ffn = 2, 128, 768, 12, 3072
     D = hd // H

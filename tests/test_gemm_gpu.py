@@ -92,6 +92,30 @@ def test_large_k_fp32_out(cuda):
     run_case(cuda, 256, 256, 8192, out=torch.float32, epi=Epilogue.BIAS)
 
 
+def test_benchmarked_16384_sampled_block(cuda):
+    """The exact bench workload (BASELINE configs[1] at 16384^3, bf16 + bias +
+    tanh-GELU, bf16 out, inputs from the device generator = the reference's
+    makeRandomTensor stream) checked on a sampled block of rows x columns
+    against the oracle on the same bf16 values (1 bf16 ulp)."""
+    import oracle as Orc
+    n = 16384
+    A = ops.fill_uniform((n, n), Orc.stream_seed("%a", 1), -1, 1, torch.bfloat16)
+    B = ops.fill_uniform((n, n), Orc.stream_seed("%b", 1), -1, 1, torch.bfloat16)
+    bias = ops.fill_uniform((n,), Orc.stream_seed("%bias", 1), -1, 1, torch.float32)
+    C = ops.gemm(A, B, bias=bias, epilogue=Epilogue.BIAS_GELU_TANH)
+    torch.cuda.synchronize()
+    rows = torch.tensor([0, 1, 255, 256, 8191, 12345, 16383])
+    cols = torch.tensor(list(range(0, 64)) + [4095, 4096, 9999, 16383])
+    a = to_host(A[rows.cuda()])
+    b = to_host(B[:, cols.cuda()])
+    want = Orc.round_to(Orc.matmul(a, b, to_host(bias[cols.cuda()]), epi=Orc.EPI_GELU_TANH,
+                                   out_t=Orc.F64), Orc.BF16)
+    got = to_host(C[rows.cuda()][:, cols.cuda()])
+    check(got, want, 2.0**-7, "bench gemm 16384^3 sampled block")
+    del A, B, C
+    torch.cuda.empty_cache()
+
+
 def test_full_size_sampled_rows_4096(cuda):
     # BASELINE configs[1] shape class at full size, parity on sampled rows
     rows = np.array([0, 1, 127, 128, 2047, 2048, 4000, 4095])
