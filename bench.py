@@ -550,6 +550,76 @@ class Attention(_Base):
         return ReferenceGraphSample("attention", threads, causal=self.causal)
 
 
+class GraphAPIGemm(_Base):
+    """The drop-in path end to end: BASELINE configs[1]'s pattern written in
+    the reference's unchanged graph API (matmul -> broadcast_in_dim(bias) ->
+    add -> the 14-nest tanh-GELU composite, bf16 values in f32 tensors, SURVEY
+    App. B) run through afg_graph_run exactly as a caller of af::interpret
+    would: host doubles in, host doubles out, every step (parse, validate,
+    device-verified pattern match, narrowing, the fused tcgen05 GEMM,
+    download). Timed on the host clock (the step includes host work by
+    definition); value = the GEMM's flops / step time."""
+
+    dtype = "bf16"
+    bound = "tensor"
+
+    def __init__(self, n=4096):
+        self.n = n
+        self.name = f"graph_api_gemm_gelu_{n}"
+
+    def config(self, world):
+        return {"workload": f"reference graph API: {self.n}^3 matmul + bias + 14-nest GELU "
+                            f"composite via afg_graph_run (host doubles in/out)",
+                "parallelism": f"replicas/{world}", "l2": "n/a (host-side step)"}
+
+    def setup(self, rank, world, dev):
+        import torch
+
+        import oracle as O
+        from oracle.graphs import matmul_epi_graph
+        self.torch = torch
+        n = self.n
+        g, fixed = matmul_epi_graph(n, n, n, "gelu")
+        self.graph = json.dumps(g)
+        self.inputs = {"a": O.round_to(O.random_tensor((n, n), "%a", 1, -1, 1), O.BF16),
+                       "b": O.round_to(O.random_tensor((n, n), "%b", 1, -1, 1), O.BF16),
+                       "bias": O.random_tensor((n,), "%bias", 1, -1, 1)}
+        self.inputs.update(fixed)
+        self.flops_rank = self.flops_total = 2.0 * n ** 3
+        self.alg_bytes_rank = 8.0 * 3 * n * n
+
+    def step(self):
+        from paper_2603_06731_b200.graph import execute
+        self.out, self.plan = execute(self.graph, self.inputs, want_plan=True)
+
+    def e2e_setup(self):
+        self.h2d = sum(v.size * 8 for v in self.inputs.values())
+        self.d2h = self.n * self.n * 8
+
+    def e2e_step(self):
+        self.step()
+
+    def reference_sample(self, threads):
+        return ReferenceGemmSample(self.n, threads)
+
+
+def measure_host(ctx, wl, steps):
+    """Host-clock timing for host-side steps (the graph API path)."""
+    wl.setup(ctx.rank, ctx.world, ctx.dev)
+    wl.step()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        wl.step()
+    ctx.barrier()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    ms_max = ctx.max_over_ranks(ms)
+    value = wl.flops_total / (ms_max * 1e-3) / 1e12
+    return {"value": value, "unit": "TFLOP/s", "ms_per_step": ms_max, "steps": steps,
+            "dtype": wl.dtype, "timing": "host clock (the step is host-side by definition)",
+            "plan": getattr(wl, "plan", None), "workload": wl.config(ctx.world)["workload"]}
+
+
 # ResNet-50 (v1.5) 3x3 / 1x1 conv layers: (H_in, C, OC, k, stride, count), BASELINE.md §5
 RESNET50 = [(56, 64, 64, 1, 1, 1), (56, 64, 64, 3, 1, 3), (56, 64, 256, 1, 1, 3),
             (56, 64, 256, 1, 1, 1), (56, 256, 64, 1, 1, 2), (56, 256, 128, 1, 1, 1),
@@ -1180,6 +1250,13 @@ def run_afg(args, wl, rank, world, local, subs=()):
         cpu = cpu_baseline(wl)
     release(wl)
     workloads = {}
+    if subs:  # the drop-in graph path, host doubles in / out (host-clock timed)
+        g = GraphAPIGemm(4096)
+        try:
+            workloads["graph_api_gemm_gelu_4096"] = measure_host(ctx, g, 3)
+        except Exception as e:
+            workloads["graph_api_gemm_gelu_4096"] = {"error": f"{type(e).__name__}: {e}"}
+        release(g)
     for name, make in subs:
         sub = make()
         try:

@@ -149,12 +149,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtArgs a) {
 // LDS.128 instead of 16 per 8 LDS.32).
 constexpr int FT = 64, FK = 16;
 
-// TX thread columns x 8 thread rows: TX = 8 -> 64 threads, 8x8 outputs each;
-// TX = 16 -> 128 threads, 8x4 each (twice the warps to hide the LDS latency).
-template <int TX>
-__global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) {
-  constexpr int T = 8 * TX;            // threads
+// TX thread columns x TY thread rows: (8, 8) -> 64 threads, 8x8 outputs each;
+// (16, 8) -> 128 threads, 8x4 each; (16, 16) -> 256 threads, 4x4 each (more
+// warps to hide the LDS latency, more LDS per FMA).
+template <int TX, int TY = 8>
+__global__ void __launch_bounds__(TY * TX) gemm_f32_blk_kernel(const SimtArgs a) {
+  constexpr int T = TY * TX;           // threads
   constexpr int CN = 64 / TX;          // columns per thread (8 or 4)
+  constexpr int RM = 64 / TY;          // rows per thread (8 or 4)
   constexpr int AK = FK * FT / T;      // A values each thread loads per slab
   constexpr int BV = FK * FT / T;      // B values each thread loads per slab
   __shared__ __align__(16) float As[2][FK][FT + 4];
@@ -165,9 +167,9 @@ __global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) 
   const int64_t bz = blockIdx.z;
   const float* A = reinterpret_cast<const float*>(a.A) + bz * a.sA;
   const float* B = reinterpret_cast<const float*>(a.B) + bz * a.sB;
-  float acc[8][CN];
+  float acc[RM][CN];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < RM; ++i)
 #pragma unroll
     for (int j = 0; j < CN; ++j) acc[i][j] = 0.0f;
 
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) 
   };
   auto frag = [&](int buf, int kk, float4& a0, float4& a1, float4& b0, float4& b1) {
     a0 = *reinterpret_cast<const float4*>(&As[buf][kk][4 * ty]);
-    a1 = *reinterpret_cast<const float4*>(&As[buf][kk][32 + 4 * ty]);
+    if constexpr (RM == 8) a1 = *reinterpret_cast<const float4*>(&As[buf][kk][32 + 4 * ty]);
     b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][4 * tx]);
     if constexpr (CN == 8) b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][32 + 4 * tx]);
   };
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) 
     const bool more = k0 + FK < a.K;
     if (more) load(k0 + FK);
     // fragments of step kk+1 are read while step kk's FMAs issue
-    float4 a0, a1, b0, b1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 a0, a1 = make_float4(0.f, 0.f, 0.f, 0.f), b0, b1 = make_float4(0.f, 0.f, 0.f, 0.f);
     frag(buf, 0, a0, a1, b0, b1);
 #pragma unroll
     for (int kk = 0; kk < FK; ++kk) {
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) 
       const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
       if (kk + 1 < FK) frag(buf, kk + 1, a0, a1, b0, b1);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < RM; ++i)
 #pragma unroll
         for (int j = 0; j < CN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(8 * TX) gemm_f32_blk_kernel(const SimtArgs a) 
   float* C = reinterpret_cast<float*>(a.C) + bz * a.sC;
   const float* R = a.residual ? reinterpret_cast<const float*>(a.residual) + bz * a.sC : nullptr;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < RM; ++i) {
     const int gm = m0 + (i < 4 ? 4 * ty + i : 32 + 4 * ty + i - 4);
     if (gm >= a.M) continue;
 #pragma unroll
@@ -333,6 +335,8 @@ afg_status gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, con
     dim3 grid((a.N + FT - 1) / FT, (a.M + FT - 1) / FT, static_cast<unsigned>(batch));
     if (variant == 64)
       gemm_f32_blk_kernel<8><<<grid, 64, 0, stream>>>(a);
+    else if (variant == 256)
+      gemm_f32_blk_kernel<16, 16><<<grid, 256, 0, stream>>>(a);
     else
       gemm_f32_blk_kernel<16><<<grid, 128, 0, stream>>>(a);
     count_launch();

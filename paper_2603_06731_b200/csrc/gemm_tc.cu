@@ -53,7 +53,18 @@ struct GemmTcArgs {
   // implicit-GEMM conv (IM2COL): output pixel m = (n, p, q) over OH x OW,
   // K = KH*KW*C ordered (ky, kx, c) like the OHWI filter.
   int c_blocks, KW, dil_w, dil_h, OH, OW, stride_w, stride_h, lower_w, lower_h;
+  int early_tmem;  // epilogue: issue the chunk's TMEM loads before the staging-buffer wait
 };
+
+// AFG_EPI_EARLY_TMEM (default: on for short-K problems): A/B switch of the
+// epilogue's TMEM-load placement
+inline int early_tmem_for(int64_t K) {
+  static const int env = [] {
+    const char* e = getenv("AFG_EPI_EARLY_TMEM");
+    return e ? atoi(e) : -1;
+  }();
+  return env >= 0 ? env : (K <= 1024 ? 1 : 0);
+}
 
 // PAIR: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile with one
 // cta_group::2 MMA per K step; each CTA stages its 128 rows of A and half of
@@ -474,14 +485,20 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
             if (has_bias) sb[rloc] = bias_v;
             bias_staged = true;
           }
-          if (live) {
+          // the chunk's TMEM columns in one round trip (all loads, one wait),
+          // issued before the wait for the staging buffer so the load latency
+          // overlaps it (the short-K epilogues stalled on that barrier)
+          uint32_t rr[CW / 32][32];
+          if (!args.early_tmem && live) {
             if (leader) tma_store_wait_read<L::EPI_BUFS - 1>();  // last store from this buffer
             epi_bar_sync(eg);
           }
-          // the chunk's TMEM columns in one round trip (all loads, one wait)
-          uint32_t rr[CW / 32][32];
 #pragma unroll
           for (int h = 0; h < CW / 32; ++h) tmem_ld32(t_row + cc * CW + h * 32, rr[h]);
+          if (args.early_tmem && live) {
+            if (leader) tma_store_wait_read<L::EPI_BUFS - 1>();  // last store from this buffer
+            epi_bar_sync(eg);
+          }
           tmem_wait_ld();
           if (cc + NG >= NCH) release_acc(acc);  // last TMEM read of the tile
 #pragma unroll
@@ -927,6 +944,7 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     return e && atoi(e) == 0;
   }();
   args.tma_store = no_tma_store ? 0 : make_store_map(&tmC, C, c, M, N, ldc);
+  args.early_tmem = early_tmem_for(K);
   cudaError_t e;
   if (pair && K >= 2048)  // long K: operand stages first (6 x 32 KB, one C buffer per group)
     e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
@@ -1008,6 +1026,7 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   cudaError_t e;
   CUtensorMap tmC;
   args.tma_store = make_store_map(&tmC, y, yt, M, OC, OC);
+  args.early_tmem = early_tmem_for(K);
   const bool f32_out = yt == AFG_F32;
 #define AFG_CONV_V(BN, ST)                                                                      \
   (dt == AFG_BF16                                                                               \
