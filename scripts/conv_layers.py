@@ -19,11 +19,12 @@ i = tot = totf = 0
 for (H, C, OC, k, s, cnt) in LAYERS:
     OH = (H + 2 * (1 if k == 3 else 0) - k) // s + 1
     f = 2 * 256 * OH * OH * OC * C * k * k
-    by = 2 * (256 * H * H * C + 256 * OH * OH * OC + OC * C * k * k)
+    x_read = 256 * OH * OH * C if (k == 1 and s > 1) else 256 * H * H * C  # strided 1x1: every s-th pixel
+    by = 2 * (x_read + 256 * OH * OH * OC + OC * C * k * k)
     t = sum(conv[i:i + cnt]) / cnt
     i += cnt
     tot += t * cnt
     totf += f * cnt
     print(f"{H:3d} {C:5d}->{OC:5d} k{k} s{s} x{cnt}: {t:7.1f} us {f / t / 1e6:7.1f} TF/s "
-          f"{by / t / 1e3:6.0f} GB/s  AI {f / by:5.0f}  floor {max(f / 1644.9e6, by / 6545e3):6.1f} us")
+          f"{by / t / 1e3:6.0f} GB/s  AI {f / by:5.0f}  floor {max(f / 1614e6, by / 6547e3):6.1f} us")
 print(f"total {tot:.1f} us, {totf / tot / 1e6:.1f} TF/s")
