@@ -355,6 +355,15 @@ typedef struct afg_graph_result afg_graph_result;
 AFG_API afg_status afg_graph_run(const char* graph_json, int n_inputs, const char* const* names,
                          const double* const* data, const int64_t* numel, int flags,
                          void* stream, afg_graph_result** out);
+/* The same, sharded over devices[0..ndev) (entries may repeat a device): one
+ * host thread per shard, the leading extent shard_extent (0: the first
+ * input's) split into contiguous blocks and propagated through the graph;
+ * GraphError if the graph mixes rows across shards (afg_graph.h GpuOptions). */
+AFG_API afg_status afg_graph_run_sharded(const char* graph_json, int n_inputs,
+                                         const char* const* names, const double* const* data,
+                                         const int64_t* numel, int flags, int ndev,
+                                         const int* devices, int64_t shard_extent,
+                                         afg_graph_result** out);
 AFG_API int afg_graph_result_count(const afg_graph_result* r);
 AFG_API const char* afg_graph_result_name(const afg_graph_result* r, int i);
 AFG_API int afg_graph_result_rank(const afg_graph_result* r, int i);

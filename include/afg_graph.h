@@ -95,6 +95,16 @@ struct GpuOptions {
   bool tensor_cores = true;   // f32 tensors holding exact bf16 / f16 values run on
                               // tcgen05 (fp32 accumulation; stated tolerance
                               // instead of bit-exactness); false = exact paths only
+  // Multi-GPU: with more than one entry the graph runs as one
+  // shard per entry on a thread-per-device group (include/afg_multi.h), the
+  // leading (batch / row) dimension of every graph input whose extent is
+  // shard_extent split into contiguous blocks; the split is propagated through
+  // the ops (elementwise, matmul rows, batch_matmul, conv batch, transposes /
+  // reshapes / reductions that keep dim 0, broadcasts into it) and outputs are
+  // concatenated back. A graph that mixes rows across shards is a GraphError
+  // ("not shardable"). Entries may repeat a device (shards then share it).
+  std::vector<int> devices;
+  int64_t shard_extent = 0;  // 0: the leading extent of the first graph input
 };
 
 struct ExecStats {

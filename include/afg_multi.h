@@ -24,7 +24,9 @@ namespace afg {
 
 class DeviceGroup {
  public:
-  explicit DeviceGroup(const std::vector<int>& devices);
+  // with_comms: create one NCCL communicator per device (ncclCommInitAll) for
+  // groups of more than one distinct device
+  explicit DeviceGroup(const std::vector<int>& devices, bool with_comms = true);
   ~DeviceGroup();
   DeviceGroup(const DeviceGroup&) = delete;
   DeviceGroup& operator=(const DeviceGroup&) = delete;

@@ -119,6 +119,10 @@ _SIGS = {
     "afg_graph_run": (_i, [ctypes.c_char_p, _i, ctypes.POINTER(ctypes.c_char_p),
                            ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
                            ctypes.POINTER(_I), _i, _P, ctypes.POINTER(_P)]),
+    "afg_graph_run_sharded": (_i, [ctypes.c_char_p, _i, ctypes.POINTER(ctypes.c_char_p),
+                                   ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
+                                   ctypes.POINTER(_I), _i, _i, ctypes.POINTER(_i), _I,
+                                   ctypes.POINTER(_P)]),
     "afg_graph_result_count": (_i, [_P]),
     "afg_graph_result_name": (ctypes.c_char_p, [_P, _i]),
     "afg_graph_result_rank": (_i, [_P, _i]),

@@ -47,6 +47,7 @@
 
 #include "../../include/afg.h"
 #include "../../include/afg_graph.h"
+#include "../../include/afg_multi.h"
 #include "afg_internal.h"
 #include "nestvm.h"
 
@@ -1886,11 +1887,169 @@ class Planner {
 
 }  // namespace
 
+namespace {
+
+// Which tensors carry the shard dimension (dim 0 split over the shards)?
+// Propagates from the graph inputs whose leading extent is B; throws a
+// GraphError when an op would mix rows of different shards.
+std::set<std::string> shard_plan(const TensorGraph& g, int64_t B) {
+  std::set<std::string> sh;
+  auto lead = [&](const std::string& id) {
+    const TensorDesc* d = g.find(id);
+    return d && !d->shape.empty() ? d->shape[0] : -1;
+  };
+  // graph inputs with leading extent B are split, except operands that must
+  // stay whole (a matmul's B, a conv filter) whose extent matches by accident
+  std::set<std::string> whole;
+  for (const auto& n : g.ops)
+    if (n.op == "matmul" || n.op == "conv2d") whole.insert(n.inputs.at(1));
+  for (const auto& id : g.inputIds())
+    if (lead(id) == B && !whole.count(id)) sh.insert(id);
+  auto no = [&](const TensorOpNode& n, const std::string& why) {
+    throw GraphError("graph not shardable along dim 0 at " + n.op + " -> " + n.output + ": " + why);
+  };
+  for (const auto& n : g.ops) {
+    const std::string& o = n.op;
+    std::vector<bool> in;
+    for (const auto& x : n.inputs) in.push_back(sh.count(x) != 0);
+    const bool any = std::find(in.begin(), in.end(), true) != in.end();
+    const bool all = std::find(in.begin(), in.end(), false) == in.end();
+    bool out = false;
+    if (o == "add" || o == "sub" || o == "mul" || o == "max" || o == "exp" || o == "quantize" ||
+        o == "dequantize") {
+      if (any && !all) no(n, "a sharded and a replicated operand");
+      out = any;
+    } else if (o == "matmul") {
+      if (in[1]) no(n, "the B operand is sharded");
+      out = in[0];
+    } else if (o == "batch_matmul" || o == "conv2d") {
+      if (o == "conv2d" && in[1]) no(n, "the filter is sharded");
+      if (o == "batch_matmul" && in[0] != in[1]) no(n, "one operand sharded");
+      out = in[0];
+    } else if (o == "transpose") {
+      if (in[0] && n.perm.at(0) != 0) no(n, "dim 0 moves");
+      out = in[0];
+    } else if (o == "broadcast_in_dim") {
+      const bool maps0 = std::find(n.dims.begin(), n.dims.end(), 0) != n.dims.end();
+      if (in[0]) {
+        if (n.dims.at(0) != 0) no(n, "dim 0 moves");
+        out = true;
+      } else {
+        // a replicated value broadcast into a [B, ...] result: each shard
+        // computes its own slice
+        out = !maps0 && lead(n.output) == B;
+      }
+    } else if (o == "reshape") {
+      if (in[0] && !(lead(n.inputs[0]) == B && lead(n.output) == B)) no(n, "dim 0 changes");
+      out = in[0];
+    } else if (o == "reduce" || o == "softmax") {
+      const int64_t r = static_cast<int64_t>(g.find(n.inputs[0])->shape.size());
+      const int64_t ax = n.axis < 0 ? n.axis + r : n.axis;
+      if (in[0] && ax == 0) no(n, "reduces over dim 0");
+      out = in[0];
+    }
+    if (out) sh.insert(n.output);
+  }
+  return sh;
+}
+
+}  // namespace
+
 std::map<std::string, TensorValue> execute(const TensorGraph& g,
                                            const std::map<std::string, TensorValue>& inputs,
                                            const GpuOptions& opt, ExecStats* stats) {
-  Planner p(g, opt, stats);
-  return p.run(inputs);
+  if (opt.devices.size() <= 1) {
+    GpuOptions o = opt;
+    int prev = -1;
+    if (opt.devices.size() == 1) {
+      cudaGetDevice(&prev);
+      cudaSetDevice(opt.devices[0]);
+    }
+    Planner p(g, o, stats);
+    auto out = p.run(inputs);
+    if (prev >= 0) cudaSetDevice(prev);
+    return out;
+  }
+  // ---- thread-per-device sharded execution ----
+  validateGraph(g);
+  const auto ins = g.inputIds();
+  int64_t B = opt.shard_extent;
+  if (B <= 0) {
+    const TensorDesc* d = ins.empty() ? nullptr : g.find(ins[0]);
+    if (!d || d->shape.empty()) throw GraphError("graph not shardable: no leading extent");
+    B = d->shape[0];
+  }
+  const int P = static_cast<int>(opt.devices.size());
+  if (B < P) throw GraphError("graph not shardable: leading extent below the device count");
+  const std::set<std::string> sh = shard_plan(g, B);
+  // contiguous blocks of the leading extent, remainder spread (shard.py)
+  std::vector<std::pair<int64_t, int64_t>> blocks;
+  for (int r = 0; r < P; ++r) {
+    const int64_t base = B / P, rem = B % P;
+    const int64_t b0 = r * base + std::min<int64_t>(r, rem);
+    blocks.push_back({b0, b0 + base + (r < rem ? 1 : 0)});
+  }
+  std::vector<TensorGraph> graphs(P, g);
+  std::vector<std::map<std::string, TensorValue>> shard_in(P);
+  for (int r = 0; r < P; ++r) {
+    const int64_t rows = blocks[r].second - blocks[r].first;
+    for (auto& t : graphs[r].tensors)
+      if (sh.count(t.id)) t.shape[0] = rows;
+    for (const auto& id : ins) {
+      auto it = inputs.find("%" + id);
+      if (it == inputs.end()) it = inputs.find(id);
+      if (it == inputs.end()) throw InterpError("missing input %" + id);
+      TensorValue v = it->second;
+      if (sh.count(id)) {
+        const int64_t inner = v.numElements() / v.shape[0];
+        v.shape[0] = rows;
+        v.data.assign(it->second.data.begin() + blocks[r].first * inner,
+                      it->second.data.begin() + blocks[r].second * inner);
+      }
+      shard_in[r]["%" + id] = std::move(v);
+    }
+  }
+  std::vector<std::map<std::string, TensorValue>> shard_out(P);
+  std::vector<std::string> errors(P);
+  std::vector<ExecStats> shard_stats(P);
+  DeviceGroup group(opt.devices, /*with_comms=*/false);  // shards exchange nothing
+  group.run([&](int r, int, void* stream, void*) {
+    try {
+      GpuOptions o = opt;
+      o.devices.clear();
+      o.stream = stream;
+      Planner p(graphs[r], o, &shard_stats[r]);
+      shard_out[r] = p.run(shard_in[r]);
+    } catch (const std::exception& e) {
+      errors[r] = e.what();
+    }
+  });
+  for (int r = 0; r < P; ++r)
+    if (!errors[r].empty()) throw InterpError("shard " + std::to_string(r) + ": " + errors[r]);
+  std::map<std::string, TensorValue> out;
+  for (const auto& [key, v0] : shard_out[0]) {
+    const std::string id = key.substr(1);
+    if (!sh.count(id)) {  // replicated: every shard computed the same value
+      out[key] = v0;
+      continue;
+    }
+    TensorValue v = v0;
+    v.shape[0] = B;
+    v.data.clear();
+    for (int r = 0; r < P; ++r) {
+      const auto& part = shard_out[r].at(key).data;
+      v.data.insert(v.data.end(), part.begin(), part.end());
+    }
+    out[key] = std::move(v);
+  }
+  if (stats)
+    for (int r = 0; r < P; ++r) {
+      for (const auto& l : shard_stats[r].plan)
+        stats->plan.push_back("[shard " + std::to_string(r) + " on device " +
+                              std::to_string(opt.devices[r]) + "] " + l);
+      stats->fused += shard_stats[r].fused;
+    }
+  return out;
 }
 
 }  // namespace gpu
@@ -1932,6 +2091,54 @@ AFG_API afg_status afg_graph_run(const char* graph_json, int n_inputs, const cha
     opt.stream = stream;
     opt.fuse = (flags & AFG_GRAPH_FUSE) != 0;
     opt.tensor_cores = (flags & AFG_GRAPH_EXACT) == 0;
+    ExecStats stats;
+    auto res = execute(g, inputs, opt, &stats);
+    auto* r = new afg_graph_result;
+    for (auto& kv : res) {
+      r->names.push_back(kv.first);
+      r->values.push_back(std::move(kv.second));
+    }
+    for (const auto& l : stats.plan) r->plan += l + "\n";
+    *out = r;
+    return AFG_OK;
+  } catch (const GraphError& e) {
+    return afg::set_error(AFG_ERR_INVALID_ARG, "GraphError: %s", e.what());
+  } catch (const InterpError& e) {
+    return afg::set_error(AFG_ERR_CUDA, "InterpError: %s", e.what());
+  } catch (const std::exception& e) {
+    return afg::set_error(AFG_ERR_INTERNAL, "%s", e.what());
+  }
+}
+
+AFG_API afg_status afg_graph_run_sharded(const char* graph_json, int n_inputs,
+                                         const char* const* names, const double* const* data,
+                                         const int64_t* numel, int flags, int ndev,
+                                         const int* devices, int64_t shard_extent,
+                                         afg_graph_result** out) {
+  using namespace afg::gpu;
+  if (!graph_json || !out || ndev < 1 || !devices || (n_inputs > 0 && (!names || !data || !numel)))
+    return afg::set_error(AFG_ERR_INVALID_ARG, "afg_graph_run_sharded: bad argument");
+  *out = nullptr;
+  try {
+    TensorGraph g = parseGraphJson(graph_json);
+    std::map<std::string, TensorValue> inputs;
+    for (int i = 0; i < n_inputs; ++i) {
+      std::string id = names[i];
+      if (!id.empty() && id[0] == '%') id.erase(0, 1);
+      const TensorDesc* d = g.find(id);
+      if (!d) throw InterpError("unknown input " + id);
+      TensorValue v;
+      v.shape = d->shape;
+      v.type = d->dtype;
+      if (v.numElements() != numel[i]) throw InterpError("input shape mismatch for %" + id);
+      v.data.assign(data[i], data[i] + numel[i]);
+      inputs["%" + id] = std::move(v);
+    }
+    GpuOptions opt;
+    opt.fuse = (flags & AFG_GRAPH_FUSE) != 0;
+    opt.tensor_cores = (flags & AFG_GRAPH_EXACT) == 0;
+    opt.devices.assign(devices, devices + ndev);
+    opt.shard_extent = shard_extent;
     ExecStats stats;
     auto res = execute(g, inputs, opt, &stats);
     auto* r = new afg_graph_result;

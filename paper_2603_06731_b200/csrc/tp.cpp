@@ -21,6 +21,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -105,7 +106,7 @@ struct DeviceGroup::Worker {
   bool stop = false, busy = false;
 };
 
-DeviceGroup::DeviceGroup(const std::vector<int>& devices) : devices_(devices) {
+DeviceGroup::DeviceGroup(const std::vector<int>& devices, bool with_comms) : devices_(devices) {
   if (devices_.empty()) throw std::invalid_argument("afg DeviceGroup: no devices");
   for (int d : devices_) {
     auto w = std::make_unique<Worker>();
@@ -134,7 +135,9 @@ DeviceGroup::DeviceGroup(const std::vector<int>& devices) : devices_(devices) {
     streams_[rank] = s;
   });
   comms_.assign(devices_.size(), nullptr);
-  if (devices_.size() > 1 && need_nccl() == AFG_OK) {
+  const bool distinct =
+      std::set<int>(devices_.begin(), devices_.end()).size() == devices_.size();
+  if (with_comms && distinct && devices_.size() > 1 && need_nccl() == AFG_OK) {
     std::vector<ncclComm_t> c(devices_.size());
     if (nccl().commInitAll(c.data(), static_cast<int>(devices_.size()), devices_.data()) ==
         ncclSuccess)

@@ -27,11 +27,13 @@ EXACT = 2
 
 
 def execute(graph, inputs: dict, fuse: bool = True, stream=None, want_plan=False,
-            exact: bool = False):
+            exact: bool = False, devices=None, shard_extent: int = 0):
     """Runs the graph on the GPU. inputs: {id or %id: array}. Returns
     {"%id": float64 array} (and the executed kernel plan if want_plan).
     fuse: kernel patterns + fused VM regions (else one launch per op);
-    exact: keep f32 tensors off the tensor cores (bit-exact paths only)."""
+    exact: keep f32 tensors off the tensor cores (bit-exact paths only);
+    devices: run sharded, one host thread per entry (the leading extent
+    shard_extent, default the first input's, split into contiguous blocks)."""
     text = graph if isinstance(graph, str) else json.dumps(graph)
     L = lib()
     names = list(inputs)
@@ -42,8 +44,13 @@ def execute(graph, inputs: dict, fuse: bool = True, stream=None, want_plan=False
     c_numel = (ctypes.c_int64 * len(names))(*[a.size for a in arrs])
     out = ctypes.c_void_p()
     flags = (FUSE if fuse else 0) | (EXACT if exact else 0)
-    st = L.afg_graph_run(text.encode(), len(names), c_names, c_data, c_numel, flags,
-                         stream, ctypes.byref(out))
+    if devices:
+        devs = (ctypes.c_int * len(devices))(*devices)
+        st = L.afg_graph_run_sharded(text.encode(), len(names), c_names, c_data, c_numel, flags,
+                                     len(devices), devs, int(shard_extent), ctypes.byref(out))
+    else:
+        st = L.afg_graph_run(text.encode(), len(names), c_names, c_data, c_numel, flags,
+                             stream, ctypes.byref(out))
     if st != 0:
         raise AfgError(st, L.afg_last_error().decode(errors="replace"))
     try:
