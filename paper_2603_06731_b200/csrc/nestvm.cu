@@ -914,6 +914,63 @@ std::string source(const Encoder& enc, const std::vector<VmBuf>& bt, const VmArg
   auto operand = [&](int32_t x) {
     return x >= 0 ? "r" + std::to_string(x) : lit(enc.consts.at(-x - 1));
   };
+  // f32 fast path. A register is "f32-exact" when every definition of it
+  // yields a value on the f32 grid (loads of f32 / f16 / bf16 / i8 buffers,
+  // roundings to those types, the fused ops below). For + - * / max of two
+  // f32-exact values immediately rounded to f32 (and used nowhere else), the
+  // interpreter's double op + roundToType(F32) equals the f32 op: double
+  // rounding through 53 bits is innocuous for these operations (53 >= 2*24+2),
+  // so the generated code uses the f32 instruction -- still bit-exact.
+  std::vector<int> uses(nreg, 0), defs_exact(nreg, 0), defs(nreg, 0);
+  auto use = [&](int32_t x) {
+    if (x >= 0 && x != INT32_MIN) ++uses[x];
+  };
+  auto grid32 = [](int t) { return t == VT_F32 || t == VT_F16 || t == VT_BF16 || t == VT_I8; };
+  for (const Ins& in : enc.code) {
+    if (in.op == OP_STORE) use(in.a);
+    if (in.op == OP_ARITH) {
+      use(in.c);
+      use(in.d);
+      use(in.e);
+    }
+  }
+  for (size_t pc = 0; pc < enc.code.size(); ++pc) {
+    const Ins& in = enc.code[pc];
+    if (in.op == OP_LOAD) {
+      ++defs[in.a];
+      defs_exact[in.a] += grid32(bt[in.b].type);
+    } else if (in.op == OP_IVVAL) {
+      ++defs[in.a];
+    } else if (in.op == OP_ARITH) {
+      ++defs[in.a];
+      const int kind = in.b & 0xff, cast = (in.b >> 8) & 0xff;
+      if ((static_cast<ArithOp>(kind) == ArithOp::Round || static_cast<ArithOp>(kind) == ArithOp::Cast) &&
+          grid32(cast))
+        ++defs_exact[in.a];
+    }
+  }
+  auto exact = [&](int32_t x) {
+    if (x == INT32_MIN) return false;
+    if (x < 0) {
+      const double v = enc.consts.at(-x - 1);
+      return static_cast<double>(static_cast<float>(v)) == v || v != v;
+    }
+    return defs[x] > 0 && defs[x] == defs_exact[x];
+  };
+  std::vector<bool> fused(enc.code.size(), false);  // arith folded into the next Round(F32)
+  for (size_t pc = 0; pc + 1 < enc.code.size(); ++pc) {
+    const Ins& in = enc.code[pc];
+    const Ins& nx = enc.code[pc + 1];
+    if (in.op != OP_ARITH || nx.op != OP_ARITH) continue;
+    const auto k = static_cast<ArithOp>(in.b & 0xff);
+    const bool f32op = k == ArithOp::Add || k == ArithOp::Sub || k == ArithOp::Mul ||
+                       k == ArithOp::Div || k == ArithOp::Max;
+    if (!f32op || static_cast<ArithOp>(nx.b & 0xff) != ArithOp::Round ||
+        ((nx.b >> 8) & 0xff) != VT_F32 || nx.c != in.a || uses[in.a] != 1 || !exact(in.c) ||
+        !exact(in.d))
+      continue;
+    fused[pc] = true;
+  }
   auto list = [&](int32_t at, const char* fn) {
     const int32_t n = enc.lists.at(at);
     std::string e = cexpr(enc.expr, enc.lists.at(at + 1));
@@ -984,6 +1041,21 @@ std::string source(const Encoder& enc, const std::vector<VmBuf>& bt, const VmArg
         const std::string x = in.c != INT32_MIN ? operand(in.c) : "0.0";
         const std::string y = in.d != INT32_MIN ? operand(in.d) : "0.0";
         const std::string z = in.e != INT32_MIN ? operand(in.e) : "0.0";
+        if (fused[pc]) {  // f32 op + Round(F32) in one f32 instruction (see above)
+          const Ins& nx = enc.code[pc + 1];
+          const std::string fx = "(float)(" + x + ")", fy = "(float)(" + y + ")";
+          std::string v;
+          switch (static_cast<ArithOp>(kind)) {
+            case ArithOp::Add: v = "__fadd_rn(" + fx + ", " + fy + ")"; break;
+            case ArithOp::Sub: v = "__fsub_rn(" + fx + ", " + fy + ")"; break;
+            case ArithOp::Mul: v = "__fmul_rn(" + fx + ", " + fy + ")"; break;
+            case ArithOp::Div: v = "__fdiv_rn(" + fx + ", " + fy + ")"; break;
+            default: v = "((" + x + ") < (" + y + ") ? " + fy + " : " + fx + ")"; break;  // Max
+          }
+          o << "    r" << nx.a << " = (double)(" << v << ");\n";
+          ++pc;  // the Round is done
+          break;
+        }
         std::string v;
         switch (static_cast<ArithOp>(kind)) {
           case ArithOp::Add: v = "__dadd_rn(" + x + ", " + y + ")"; break;
