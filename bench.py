@@ -180,12 +180,16 @@ class GemmBF16:
     def __init__(self, size):
         self.n = size
         self.name = f"gemm_bf16_gelu_{size}"  # per-size traffic entry in profiles/traffic.json
+        # A, B and C fit in the 126 MB L2 up to 4096^2: flush between steps
+        self.flushed = 3 * 2 * size * size < 2 * 126e6 and not os.environ.get("AFG_BENCH_NO_FLUSH")
+        self.flush = None
 
     def config(self, world):
         return {"workload": f"bf16 matmul {self.n}x{self.n}x{self.n} + bias + tanh-GELU "
                             f"epilogue (fp32 accumulate), row-sharded",
                 "M": self.n, "N": self.n, "K": self.n, "parallelism": f"rows/{world}",
-                "l2": "operands larger than L2 (no flush needed)",
+                "l2": ("operands larger than L2 (no flush needed)" if not self.flushed else
+                       "L2 flushed between steps (256 MB write + 256 MB read, untimed)"),
                 "sweep": "2048-16384 via --size"}
 
     metric = "TFLOP/s"
@@ -209,6 +213,9 @@ class GemmBF16:
         self.bias = ops.fill_uniform((self.n,), oracle.stream_seed("%bias", 1), -1, 1,
                                      torch.float32)
         self.C = torch.empty((self.m, self.n), dtype=torch.bfloat16, device=dev)
+        if self.flushed:
+            self.flush = L2Flush(dev)
+            self.pre_step = self.flush
         self.flops_rank = 2.0 * self.m * self.n * self.n
         self.flops_total = 2.0 * self.n ** 3
         self.alg_bytes_rank = 2.0 * (self.m * self.n + self.n * self.n + self.m * self.n) + 4 * self.n

@@ -54,7 +54,24 @@ struct GemmTcArgs {
   // K = KH*KW*C ordered (ky, kx, c) like the OHWI filter.
   int c_blocks, KW, dil_w, dil_h, OH, OW, stride_w, stride_h, lower_w, lower_h;
   int early_tmem;  // epilogue: issue the chunk's TMEM loads before the staging-buffer wait
+  int round_sync;  // 0: off; else 1 + counter slot: producers hold tile round r+1
+                   // until every CTA has issued round r (bounded wait)
 };
+
+// Round sync counters, one pair per slot (the host picks the slot from the
+// stream, so concurrent launches on different streams do not share one):
+// [0] = CTA arrivals per tile round, [1] = kernel exits. The last CTA to exit
+// resets both; the next launch on the stream touches them only after
+// griddepcontrol.wait (the previous grid has completed). A wait is bounded, so
+// a disturbed counter costs time, never correctness or progress.
+constexpr int ROUND_SLOTS = 64;
+__device__ unsigned int g_round[ROUND_SLOTS][2];
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // AFG_EPI_EARLY_TMEM (default: on for short-K problems): A/B switch of the
 // epilogue's TMEM-load placement
@@ -64,6 +81,23 @@ inline int early_tmem_for(int64_t K) {
     return e ? atoi(e) : -1;
   }();
   return env >= 0 ? env : (K <= 1024 ? 1 : 0);
+}
+
+// Round sync for problems of several tile rounds: the persistent clusters
+// otherwise drift apart in K, and the CTAs sharing an A / B panel read it from
+// DRAM at different times (16384^3: 20.3 GB DRAM read per launch, 6.59 ms;
+// with the sync 8.8 GB, 5.80 ms -- the saved DRAM power shows up as clock on
+// the power-capped chip). AFG_GEMM_ROUND_SYNC=0 turns it off (A/B).
+// Short K (rounds of a few microseconds) loses more to the wait than it saves
+// (ResNet 1x1 convs: 747 -> 681 TFLOP/s), so only K >= 4096 syncs.
+inline int round_sync_for(int tiles, int64_t K, bool pair, cudaStream_t stream) {
+  static const int env = [] {
+    const char* e = getenv("AFG_GEMM_ROUND_SYNC");
+    return e ? atoi(e) : 1;
+  }();
+  if (env <= 0 || K < 4096 || tiles < 4 * (pair ? num_sms() / 2 : num_sms())) return 0;
+  const uintptr_t h = reinterpret_cast<uintptr_t>(stream);
+  return 1 + static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % ROUND_SLOTS);
 }
 
 // PAIR: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile with one
@@ -317,7 +351,18 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < num_tiles; t += ncl) {
+      int round = 0;
+      unsigned int* ctr = args.round_sync ? g_round[args.round_sync - 1] : nullptr;
+      for (int t = cid; t < num_tiles; t += ncl, ++round) {
+        if (ctr && round > 0) {
+          // hold this round's loads until every CTA has issued the previous
+          // round's: the clusters of a wave stay in K-lockstep, so each panel
+          // slice is read from DRAM once per wave (bounded: never a deadlock)
+          const unsigned int want = static_cast<unsigned int>(round) * gridDim.x;
+          const uint64_t t0 = global_ns();
+          while (ld_acquire_gpu(&ctr[0]) < want && global_ns() - t0 < 20000) {
+          }
+        }
         int mb, nb;
         tile_coords(t, args.num_m_blocks, args.num_n_blocks, args.group_m, mb, nb);
         const int m0 = mb * TILE_M + static_cast<int>(rank) * BLOCK_M;
@@ -367,6 +412,7 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
             phase ^= 1;
           }
         }
+        if (ctr) atomicAdd(&ctr[0], 1u);
       }
     }
   } else if (warp == 1) {
@@ -567,6 +613,15 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
     else tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+  if (args.round_sync && threadIdx.x == 0) {
+    unsigned int* ctr = g_round[args.round_sync - 1];
+    __threadfence();
+    if (atomicAdd(&ctr[1], 1u) == gridDim.x - 1) {  // last CTA out: reset for the next launch
+      atomicExch(&ctr[0], 0u);
+      atomicExch(&ctr[1], 0u);
+      __threadfence();
+    }
   }
 }
 
@@ -891,6 +946,16 @@ bool four_epi_groups(afg_epilogue epi) {
   return epi == AFG_EPI_BIAS_GELU_TANH || epi == AFG_EPI_BIAS_GELU_ERF;
 }
 
+// AFG_GEMM_SHORTK_GROUPS = 2 | 4: epilogue groups of the output-bound
+// (K <= 128, BLOCK_N = 256) single-CTA GEMM
+int shortk_groups() {
+  static const int g = [] {
+    const char* e = getenv("AFG_GEMM_SHORTK_GROUPS");
+    return e ? atoi(e) : 4;
+  }();
+  return g;
+}
+
 }  // namespace
 
 // Entry used by afg_gemm (api.cpp) and the conv / BERT paths.
@@ -904,11 +969,17 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     const char* e = getenv("AFG_GEMM_BN");
     return e ? atoi(e) : 0;
   }();
-  const int block_n = (bn_env == 64 || bn_env == 128 || bn_env == 256)
-                          ? bn_env
-                          : (N >= 256 ? 256 : (N > 64 ? 128 : 64));
+  int block_n = (bn_env == 64 || bn_env == 128 || bn_env == 256)
+                    ? bn_env
+                    : (N >= 256 ? 256 : (N > 64 ? 128 : 64));
   // 256 x 256 tiles on a CTA pair when there are enough of them to fill the GPU
   const bool pair = use_pair_tiles(block_n, M, N, K);
+  // fewer 128 x 256 tiles than SMs (2048^3: 128 tiles): 128 x 128 tiles, so
+  // that the SMs with two tiles overlap one tile's epilogue with the other's
+  // main loop (2048^3 + GELU, L2 flushed: 32.6 -> 26.7 us)
+  if (!pair && bn_env == 0 && block_n == 256 && K >= 1024 &&
+      ((M + BLOCK_M - 1) / BLOCK_M) * ((N + 255) / 256) < num_sms())
+    block_n = 128;
   const CUtensorMapDataType tdt =
       ab == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmA, tmB;
@@ -945,6 +1016,7 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   }();
   args.tma_store = no_tma_store ? 0 : make_store_map(&tmC, C, c, M, N, ldc);
   args.early_tmem = early_tmem_for(K);
+  args.round_sync = round_sync_for(args.num_m_blocks * args.num_n_blocks, K, pair, stream);
   cudaError_t e;
   if (pair && K >= 2048)  // long K: operand stages first (6 x 32 KB, one C buffer per group)
     e = dispatch_types<256, 6, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
@@ -952,6 +1024,10 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     e = dispatch_types<256, 5, true, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (pair)  // shorter K: the epilogue matters more (5 stages, two C buffers per group)
     e = dispatch_types<256, 5, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
+  // output-bound: 2 stages; 4 epilogue groups x 2 C buffers (ResNet 56x56
+  // 64 -> 256 1x1: 103.6 -> 90.2 us vs 2 groups x 4 buffers)
+  else if (block_n == 256 && K <= 128 && shortk_groups() == 4)
+    e = dispatch_types<256, 2, false, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 256 && K <= 128)  // output-bound: 2 stages, 4 C buffers per group
     e = dispatch_types<256, 2>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 256)
@@ -1027,6 +1103,7 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
   CUtensorMap tmC;
   args.tma_store = make_store_map(&tmC, y, yt, M, OC, OC);
   args.early_tmem = early_tmem_for(K);
+  args.round_sync = 0;  // measured: ResNet convs 747 -> 681 TFLOP/s with it
   const bool f32_out = yt == AFG_F32;
 #define AFG_CONV_V(BN, ST)                                                                      \
   (dt == AFG_BF16                                                                               \
