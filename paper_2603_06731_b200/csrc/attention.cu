@@ -63,10 +63,18 @@ struct AttnArgs {
   const int* sched;
   const int* sched_off;
   const int* sched_cnt;
+  int dyn;         // 0: static snake; else 1 + counter slot: units taken from a global
+                   // atomic queue in `decode` order by whichever CTA is free
   int o_st32;      // 16-bit O rows 32-byte aligned: 256-bit stores
   int dbg;  // profiling aid (AFG_ATTN_DEBUG): 1 = no softmax math, 2 = no MMAs,
            // 3 = MMAs back to back (no softmax dependency)
 };
+
+// Dynamic unit queue, one counter pair per slot (the host picks the slot from
+// the stream): [0] = next unit, [1] = CTA exits; the last CTA out resets both
+// and the next launch on the stream touches them after griddepcontrol.wait.
+constexpr int ATTN_SLOTS = 64;
+__device__ unsigned int g_attn_queue[ATTN_SLOTS][2];
 
 template <int D>
 struct AttnSmem {
@@ -84,9 +92,10 @@ struct AttnSmem {
   static constexpr int RING_OFF = QBUF * QBUF_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * TILE;
   // q_full[QBUF], q_empty[QBUF], kv_full[S], kv_empty[S], s_full[2], p_full[2][2],
-  // o_full[2], o_empty[2]
-  static constexpr int NUM_BARS = 2 * QBUF + 2 * STAGES + 10;
-  static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 1024;
+  // o_full[2], o_empty[2], unit_full[UNIT_R], unit_empty[UNIT_R]
+  static constexpr int UNIT_R = 4;  // dynamic schedule: unit ids in flight (TMA -> MMA, softmax)
+  static constexpr int NUM_BARS = 2 * QBUF + 2 * STAGES + 10 + 2 * UNIT_R;
+  static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 4 * UNIT_R + 1024;
   static_assert(TOTAL <= 232448, "attention smem over the 227 KB opt-in limit");
 };
 
@@ -173,7 +182,10 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_full = s_full + 2;     // [tile][half]: P columns of keys [0,64) / [64,128)
   uint64_t* o_full = p_full + 4;     // [2]
   uint64_t* o_empty = o_full + 2;    // [2]
+  uint64_t* unit_full = o_empty + 2;               // [UNIT_R]
+  uint64_t* unit_empty = unit_full + L::UNIT_R;    // [UNIT_R]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
+  int* unit_ring = reinterpret_cast<int*>(tmem_slot + 4);  // [UNIT_R]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -186,7 +198,18 @@ __global__ void __launch_bounds__(384, 1)
   // Linear order: heads in groups of HEAD_GROUP; inside a group the query-tile
   // pairs run from the last (heaviest under causal masking) down, all heads of
   // the group per pair (co-resident CTAs share the group's K/V in L2).
+  // dynamic schedule, consumer side (MMA warp, softmax warps): the unit id the
+  // TMA warp fetched for this CTA's u-th unit; one release arrival per warp
+  auto unit_take = [&](int u) {
+    const int slot = u % L::UNIT_R;
+    mbar_wait(&unit_full[slot], (u / L::UNIT_R) & 1);
+    const int lin = *reinterpret_cast<volatile int*>(&unit_ring[slot]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&unit_empty[slot]);
+    return lin;
+  };
   auto unit_of = [&](int u) {
+    if (args.dyn) return unit_take(u);
     if (args.sched) {  // host-balanced list of unit codes
       return u < args.sched_cnt[blockIdx.x] ? args.sched[args.sched_off[blockIdx.x] + u] : n_units;
     }
@@ -240,6 +263,10 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&o_full[g], 1);
       mbar_init(&o_empty[g], 4);
     }
+    for (int r = 0; r < L::UNIT_R; ++r) {
+      mbar_init(&unit_full[r], 1);
+      mbar_init(&unit_empty[r], 9);  // the MMA warp + 8 softmax warps
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -290,11 +317,18 @@ __global__ void __launch_bounds__(384, 1)
           warp_arrive(&p_full[2 * g + 1]);
           continue;
         }
-        // the whole S row (128 fp32 scores) into registers with one TMEM pass
-        uint32_t s[NCH][32];
+        // the whole S row (128 fp32 scores) into registers with one TMEM pass,
+        // as 64 column pairs (the f32x2 math below takes them directly)
+        uint64_t sp[NCH][16];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) tmem_ld32(s_base + c * 32, s[c]);
+        for (int c = 0; c < NCH; ++c) tmem_ld32x2(s_base + c * 32, sp[c]);
         tmem_wait_ld();
+        auto lo = [](uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x)); };
+        auto hi = [](uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x >> 32)); };
+        auto pk = [](float a, float b) {
+          return static_cast<uint64_t>(__float_as_uint(a)) |
+                 (static_cast<uint64_t>(__float_as_uint(b)) << 32);
+        };
         const int k0 = j * BN;
         const bool need_mask = (args.causal && k0 + BN - 1 > tile_first) || k0 + BN > args.Nk;
         // Common path (no additive bias, scale > 0): the max is taken on the raw
@@ -310,18 +344,20 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int c = 0; c < NCH; ++c)
 #pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (c * 32 + e >= lim) s[c][e] = 0xff800000u;  // -inf
+              for (int e = 0; e < 16; ++e) {
+                const int col = c * 32 + 2 * e;
+                sp[c][e] = pk(col >= lim ? -INFINITY : lo(sp[c][e]),
+                              col + 1 >= lim ? -INFINITY : hi(sp[c][e]));
+              }
           }
           float mc[NCH];
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            mc[c] = fmax3(__uint_as_float(s[c][0]), __uint_as_float(s[c][1]),
-                          __uint_as_float(s[c][2]));
+            mc[c] = fmax3(lo(sp[c][0]), hi(sp[c][0]), lo(sp[c][1]));
+            mc[c] = fmax3(mc[c], hi(sp[c][1]), lo(sp[c][2]));
 #pragma unroll
-            for (int e = 3; e < 31; e += 2)
-              mc[c] = fmax3(mc[c], __uint_as_float(s[c][e]), __uint_as_float(s[c][e + 1]));
-            mc[c] = fmaxf(mc[c], __uint_as_float(s[c][31]));
+            for (int e = 2; e < 15; ++e) mc[c] = fmax3(mc[c], hi(sp[c][e]), lo(sp[c][e + 1]));
+            mc[c] = fmaxf(mc[c], hi(sp[c][15]));
           }
           tmax = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])) * args.scale_log2;
           sc = args.scale_log2;
@@ -330,13 +366,18 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int kj = k0 + c * 32 + e;
-              float v = __uint_as_float(s[c][e]) * args.scale_log2;
-              if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
-              if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
-              s[c][e] = __float_as_uint(v);
-              tmax = fmaxf(tmax, v);
+            for (int e = 0; e < 16; ++e) {
+              float v2[2] = {lo(sp[c][e]), hi(sp[c][e])};
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int kj = k0 + c * 32 + 2 * e + h;
+                float v = v2[h] * args.scale_log2;
+                if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
+                if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
+                v2[h] = v;
+                tmax = fmaxf(tmax, v);
+              }
+              sp[c][e] = pk(v2[0], v2[1]);
             }
           sc = 1.0f;
         }
@@ -364,15 +405,14 @@ __global__ void __launch_bounds__(384, 1)
         m = m_new;
         // P = exp2(sc * s - base) packed to 16 bit, written over S (P chunk c
         // lands in columns 16c..16c+15; the scores are already in registers)
-        const uint64_t sc2 = f2(sc, sc), nb2 = f2(-base, -base);
+        const uint64_t sc2 = pk(sc, sc), nb2 = pk(-base, -base);
         uint64_t acc2[2] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f)};  // two chains: half the add latency
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const uint64_t x2 =
-                ffma2(f2(__uint_as_float(s[c][2 * e]), __uint_as_float(s[c][2 * e + 1])), sc2, nb2);
+            const uint64_t x2 = ffma2(sp[c][e], sc2, nb2);
             float p0, p1;
             // pairs selected by POLY_PAIRS run on the FMA pipe, the rest on MUFU
             if ((POLY_PAIRS >> (e % 8)) & 1) {
@@ -455,13 +495,25 @@ __global__ void __launch_bounds__(384, 1)
       // ------------------------------------------------------------- TMA --
       if (lane == 0) {
         int n = 0;  // K/V ring item counter across units (item 2j = K(j), 2j+1 = V(j))
+        unsigned int* queue = args.dyn ? g_attn_queue[args.dyn - 1] : nullptr;
         for (int u = 0;; ++u) {
-          const int lin = unit_of(u);
-          if (lin >= n_units) break;
-          const Unit w = decode(lin);
           const int qb = u % QBUF;
           // the S MMAs of the unit that last used this Q buffer are done
           mbar_wait(&q_empty[qb], ((u / QBUF) & 1) ^ 1);
+          int lin;
+          if (queue) {
+            // take the next unit only now that its Q tiles can load: a CTA
+            // never holds more than the unit it is about to start
+            const int slot = u % L::UNIT_R;
+            mbar_wait(&unit_empty[slot], ((u / L::UNIT_R) & 1) ^ 1);
+            lin = min(static_cast<int>(atomicAdd(&queue[0], 1u)), n_units);
+            unit_ring[slot] = lin;
+            mbar_arrive(&unit_full[slot]);
+          } else {
+            lin = unit_of(u);
+          }
+          if (lin >= n_units) break;
+          const Unit w = decode(lin);
           mbar_arrive_expect_tx(&q_full[qb], 2 * L::TILE);
           for (int g = 0; g < 2; ++g)
             for (int a = 0; a < DB; ++a)
@@ -588,6 +640,15 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem);
+  }
+  if (args.dyn && threadIdx.x == 0) {
+    unsigned int* queue = g_attn_queue[args.dyn - 1];
+    __threadfence();
+    if (atomicAdd(&queue[1], 1u) == gridDim.x - 1) {  // last CTA out: reset for the next launch
+      atomicExch(&queue[0], 0u);
+      atomicExch(&queue[1], 0u);
+      __threadfence();
+    }
   }
 }
 
@@ -732,7 +793,10 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
     return e ? atoi(e) : 0;
   }();
   a.sched = a.sched_off = a.sched_cnt = nullptr;
-  if (sched_env) {
+  if (a.dyn) {
+    const uintptr_t h = reinterpret_cast<uintptr_t>(s);
+    a.dyn = 1 + static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % ATTN_SLOTS);
+  } else if (sched_env) {
     const Sched& sc = attn_schedule(a.BH, a.Nq, a.Nk, D, a.causal, static_cast<int>(grid));
     if (sc.dev) {
       a.sched = sc.dev;
@@ -833,7 +897,18 @@ afg_status attention_core(const void* q, const void* k, const void* v, const flo
       const char* e = getenv("AFG_ATTN_HEAD_GROUP");
       return e ? atoi(e) : 0;
     }();
-    a.head_group = hg_env > 0 ? hg_env : (causal ? static_cast<int>(BH) : 16);
+    // AFG_ATTN_DYN=0: the static snake walk. The dynamic queue balances the
+    // CTAs by their actual unit times, so causal units can stay grouped by
+    // heads whose K / V fit in L2 without unbalancing the tail.
+    static const int dyn_env = [] {
+      const char* e = getenv("AFG_ATTN_DYN");
+      return e ? atoi(e) : 1;
+    }();
+    a.dyn = dyn_env;
+    // Measured at B8H16S2048D128 causal: 171.6 us static / all heads, 157-158
+    // us dynamic with groups of 16 or 32 heads (K/V DRAM reads 513 -> 202 MB),
+    // 164 us with groups of 8.
+    a.head_group = hg_env > 0 ? hg_env : (a.dyn || !causal ? 16 : static_cast<int>(BH));
     cudaError_t e;
     if (D == 128)
       e = dt == AFG_BF16 ? launch_tc<128, true>(tq, tk, tv, a, s) : launch_tc<128, false>(tq, tk, tv, a, s);
