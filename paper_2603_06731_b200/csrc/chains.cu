@@ -266,12 +266,29 @@ __device__ __forceinline__ uint32_t pack_pair(uint64_t v) {
   }
 }
 
+// Tail balancing: the last `pool` rows are not assigned to a CTA; producers
+// claim them slot by slot from a global counter (one pair per stream slot:
+// [0] = rows claimed, [1] = producer exits; the last producer out resets both,
+// the next launch touches them after griddepcontrol.wait). The per-SM DRAM
+// rates differ, so a static split ends with the slowest SM alone (layernorm:
+// SM active 45.4 k cycles on average, 48.7 k at most).
+constexpr int ROW_SLOTS = 64;
+__device__ unsigned int g_row_pool[ROW_SLOTS][2];
+
+// What a ring slot holds: rows [row, row + n) (n > 0), nothing (n = 0: skip
+// it), or the end of the stream for the consumer warp that reads it (n < 0).
+struct SlotDesc {
+  int64_t row;
+  int n, pad;
+};
+
 template <typename TI, typename TO, int MODE, int CH>  // MODE 0 softmax, 1 layernorm
 __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     stream_rows_kernel(const TI* __restrict__ x, const TI* __restrict__ res,
                        const float* __restrict__ gamma, const float* __restrict__ beta,
                        TO* __restrict__ y, TO* __restrict__ sum_out, int64_t rows, int cols,
-                       float eps, int ns, int slot_bytes, int grp) {
+                       float eps, int ns, int slot_bytes, int grp, unsigned int* pool_ctr,
+                       int64_t pool) {
   using namespace sm100;
   constexpr int E = Vec<TI>::N;
   extern __shared__ uint8_t smem_raw[];
@@ -279,11 +296,13 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
                                              ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(ns) * slot_bytes);
   uint64_t* empty = full + ns;
-  float* gb = reinterpret_cast<float*>(empty + ns);  // layernorm: gamma | beta
+  SlotDesc* desc = reinterpret_cast<SlotDesc*>(empty + ns);
+  float* gb = reinterpret_cast<float*>(desc + ns + 2);  // layernorm: gamma | beta
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t srows = rows - pool;  // statically split rows
+  const int64_t per = (srows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * per;
-  const int64_t nr = max(static_cast<int64_t>(0), min(per, rows - r0));
+  const int64_t nr = max(static_cast<int64_t>(0), min(per, srows - r0));
   // a ring slot holds `grp` consecutive rows (of x, then of the residual):
   // fewer, larger bulk copies (the per-copy cost bounds 1.5 KB rows)
   const int64_t nslots = (nr + grp - 1) / grp;
@@ -293,6 +312,9 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
+    desc[ns].row = -1;  // producer control words (see the producer)
+    desc[ns].n = 0;
+    desc[ns + 1].row = -1;
     fence_barrier_init();
   }
   __syncthreads();  // barriers initialised: the producer starts streaming at once
@@ -315,24 +337,121 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     // (Issuing in warp-wide lock-step batches of `ns` rows drained the whole
     // ring before each refill -- on the 151 MB layernorm the DRAM read rate
     // stayed at ~3.6 TB/s.) One lane owning a slot means no wait can see a
-    // phase two laps stale.
-    for (int64_t k = 0;; ++k) {
-      bool issued = false;
-      for (int slot = lane; slot < ns; slot += 32) {
-        const int64_t i = static_cast<int64_t>(k) * ns + slot;
-        if (i >= nslots) break;
-        issued = true;
-        const int64_t row = i * grp;
-        const uint32_t bytes =
-            static_cast<uint32_t>(min(static_cast<int64_t>(grp), nr - row)) * row_bytes;
-        mbar_wait(&empty[slot], static_cast<uint32_t>(k & 1) ^ 1u);
+    // phase two laps stale. Stream index i = k * ns + slot: the CTA's static
+    // rows first, then rows claimed from the pool; the first index a lane
+    // cannot fill becomes a skip. With B = the largest such index in the
+    // warp, every index <= B is then data or a skip and (B, B + STREAM_WARPS]
+    // -- one index per consumer warp -- holds the end marker.
+    int64_t k = 0;
+    int sj = 0;  // this lane's slot = lane + 32 sj
+    auto advance_p = [&]() {
+      if (lane + 32 * (++sj) >= ns) {
+        sj = 0;
+        ++k;
+      }
+    };
+    auto fill = [&](int64_t i, int64_t row, int n) {
+      const int slot = static_cast<int>(i - k * ns);
+      mbar_wait(&empty[slot], static_cast<uint32_t>(k & 1) ^ 1u);
+      desc[slot].row = row;
+      desc[slot].n = n;
+      if (n > 0) {
+        const uint32_t bytes = static_cast<uint32_t>(n) * row_bytes;
         uint8_t* dst = smem + static_cast<size_t>(slot) * slot_bytes;
         mbar_arrive_expect_tx(&full[slot], MODE == 1 && res ? 2 * bytes : bytes);
-        bulk_load(dst, x + (r0 + row) * cols, bytes, &full[slot]);
-        if (MODE == 1 && res)
-          bulk_load(dst + grp * row_bytes, res + (r0 + row) * cols, bytes, &full[slot]);
+        bulk_load(dst, x + row * cols, bytes, &full[slot]);
+        if (MODE == 1 && res) bulk_load(dst + grp * row_bytes, res + row * cols, bytes, &full[slot]);
+      } else {
+        mbar_arrive(&full[slot]);
       }
-      if (!issued) break;
+    };
+    // ctl[0].row: the highest index any lane has started to fill; ctl[1].row:
+    // the highest exhaustion index; ctl[0].n: lanes exhausted. An exhausted
+    // lane fills skips only below the highest started index (every index a
+    // blocked fill transitively waits for lies below it), and places the end
+    // markers once all lanes are exhausted -- no warp-wide barrier, which
+    // could wait on a lane whose fill waits on a skip of the waiting lane.
+    SlotDesc* ctl = desc + ns;
+    auto* prog = reinterpret_cast<long long*>(&ctl[0].row);
+    auto* bexh = reinterpret_cast<long long*>(&ctl[1].row);
+    const bool use_pool = pool_ctr != nullptr && pool > 0;
+    if (!use_pool) {
+      // static rows only: the consumers know the count, no markers needed
+      for (;;) {
+        const int64_t i = k * ns + lane + 32 * sj;
+        if (lane >= ns || i >= nslots) break;
+        fill(i, r0 + i * grp, static_cast<int>(min(static_cast<int64_t>(grp), nr - i * grp)));
+        advance_p();
+      }
+      return;
+    }
+    if (lane < ns) {
+      // the pool claim for a lane's next dynamic fill is issued right after
+      // the previous fill, so its round trip overlaps the wait for the slot
+      unsigned int claim = 0;
+      bool claimed = false;
+      // a claim past the pool end is answered by a plain load once the pool is
+      // drained: every lane's final (failing) claim would otherwise queue on
+      // the one counter behind the real ones
+      auto claim_rows = [&]() -> unsigned int {
+        const unsigned int seen = *reinterpret_cast<volatile unsigned int*>(&pool_ctr[0]);
+        if (seen >= static_cast<unsigned int>(pool)) return seen;
+        return atomicAdd(&pool_ctr[0], static_cast<unsigned int>(grp));
+      };
+      for (;;) {
+        const int64_t i = k * ns + lane + 32 * sj;
+        int64_t row = 0;
+        int n = 0;
+        if (i < nslots) {
+          row = r0 + i * grp;
+          n = static_cast<int>(min(static_cast<int64_t>(grp), nr - i * grp));
+        } else if (use_pool) {
+          if (!claimed) claim = claim_rows();
+          claimed = false;
+          row = srows + static_cast<int64_t>(claim);
+          n = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(grp), rows - row)));
+        }
+        atomicMax(prog, static_cast<long long>(i));
+        fill(i, row, n);
+        advance_p();
+        if (n == 0) {
+          atomicMax(bexh, static_cast<long long>(i));
+          __threadfence_block();
+          atomicAdd(&ctl[0].n, 1);
+          break;
+        }
+        if (use_pool && k * ns + lane + 32 * sj >= nslots) {
+          claim = claim_rows();
+          claimed = true;
+        }
+      }
+      const int lanes = ns < 32 ? ns : 32;
+      for (;;) {
+        const int64_t i = k * ns + lane + 32 * sj;
+        if (*reinterpret_cast<volatile int*>(&ctl[0].n) == lanes) break;
+        if (i < *reinterpret_cast<volatile long long*>(prog)) {
+          fill(i, 0, 0);
+          advance_p();
+        } else {
+          __nanosleep(64);
+        }
+      }
+      __threadfence_block();
+      const int64_t bmax = *reinterpret_cast<volatile long long*>(bexh);
+      for (;;) {
+        const int64_t i = k * ns + lane + 32 * sj;
+        if (i > bmax + STREAM_WARPS) break;
+        fill(i, 0, i <= bmax ? 0 : -1);
+        advance_p();
+      }
+    }
+    if (pool_ctr != nullptr && lane == 0) {
+      __threadfence();
+      if (atomicAdd(&pool_ctr[1], 1u) == gridDim.x - 1) {  // last producer out: reset
+        atomicExch(&pool_ctr[0], 0u);
+        atomicExch(&pool_ctr[1], 0u);
+        __threadfence();
+      }
     }
     return;
   }
@@ -341,7 +460,11 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
   // slot: ns is a multiple of STREAM_WARPS, so it wraps exactly
   int cslot = warp;
   uint32_t cph = 0;
+  int64_t ci = warp;  // stream index of the slot this warp reads next
+  // without a pool the stream is the CTA's static slots: stop after them
+  const int64_t cend = pool_ctr != nullptr && pool > 0 ? INT64_MAX : nslots;
   auto advance = [&]() {
+    ci += STREAM_WARPS;
     cslot += STREAM_WARPS;
     if (cslot >= ns) {
       cslot -= ns;
@@ -350,11 +473,19 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
   };
   const float inv_cols = 1.0f / static_cast<float>(cols);
   if constexpr (MODE == 0) {
-    for (int64_t i = warp; i < nr; i += STREAM_WARPS, advance()) {
+    for (;; advance()) {
+      if (ci >= cend) break;
       const int slot = cslot;
       mbar_wait(&full[slot], cph);
+      const int dn = reinterpret_cast<volatile SlotDesc*>(desc)[slot].n;
+      if (dn < 0) break;  // end of this warp's stream
+      if (dn == 0) {      // skip
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        continue;
+      }
       const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
-      const int64_t row = r0 + i;
+      const int64_t row = reinterpret_cast<volatile SlotDesc*>(desc)[slot].row;
       TO* yr = y + row * cols;
       Vec<TI> raw[CH];
         float mx = -INFINITY;
@@ -432,16 +563,24 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
           gp[k][p] = sm100::f2(greg[k][2 * p], greg[k][2 * p + 1]);
           bp[k][p] = sm100::f2(breg[k][2 * p], breg[k][2 * p + 1]);
         }
-      for (int64_t si = warp; si < nslots; si += STREAM_WARPS, advance()) {
+      for (;; advance()) {
+        if (ci >= cend) break;
         const int slot = cslot;
         mbar_wait(&full[slot], cph);
+        const int dn = reinterpret_cast<volatile SlotDesc*>(desc)[slot].n;
+        if (dn < 0) break;  // end of this warp's stream
+        if (dn == 0) {      // skip
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+          continue;
+        }
+        const int64_t row0 = reinterpret_cast<volatile SlotDesc*>(desc)[slot].row;
         const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
-        const int64_t i0 = si * R;
         uint64_t v[R][CH][E / 2];
         bool have[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          have[r] = i0 + r < nr;
+          have[r] = r < dn;
 #pragma unroll
           for (int k = 0; k < CH; ++k) {
             const int c = lane + 32 * k;
@@ -509,7 +648,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!have[r]) continue;
-          const int64_t row = r0 + i0 + r;
+          const int64_t row = row0 + r;
           // y = ((v - mean) * rstd) * g + b = (v * rstd + (-mean * rstd)) * g + b
           const uint64_t ra = sm100::f2(rstd[r], rstd[r]);
           const float c0 = -mean[r] * rstd[r];
@@ -532,16 +671,24 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
         }
       }
     } else {
-    for (int64_t si = warp; si < nslots; si += STREAM_WARPS, advance()) {
+    for (;; advance()) {
+      if (ci >= cend) break;
       const int slot = cslot;
       mbar_wait(&full[slot], cph);
+      const int dn = reinterpret_cast<volatile SlotDesc*>(desc)[slot].n;
+      if (dn < 0) break;  // end of this warp's stream
+      if (dn == 0) {      // skip
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        continue;
+      }
+      const int64_t row0 = reinterpret_cast<volatile SlotDesc*>(desc)[slot].row;
       const uint32_t sx = smem_u32(smem + static_cast<size_t>(slot) * slot_bytes);
-      const int64_t i0 = si * R;
       float v[R][CH][E];
       bool have[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        have[r] = i0 + r < nr;
+        have[r] = r < dn;
         if (!have[r]) continue;
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -641,7 +788,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!have[r]) continue;
-          const int64_t row = r0 + i0 + r;
+          const int64_t row = row0 + r;
           Vec<TO> o, so;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
@@ -688,7 +835,35 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   const int ns = static_cast<int>(std::min<int64_t>(90, budget / slot_bytes)) /
                  STREAM_WARPS * STREAM_WARPS;
   if (ns < STREAM_WARPS || rows < 8ll * num_sms()) return cudaErrorNotSupported;
-  const int smem = ns * slot_bytes + ns * 16 + 128 + (MODE == 1 ? static_cast<int>(cols) * 8 + 16 : 0);
+  const int smem = ns * slot_bytes + ns * 16 + (ns + 2) * static_cast<int>(sizeof(SlotDesc)) + 128 +
+                   (MODE == 1 ? static_cast<int>(cols) * 8 + 16 : 0);
+  // tail pool (AFG_STREAM_POOL = denominator, 0 = off). Measured: softmax
+  // [262144, 2048] 370 -> 333 us with 1/4 of the rows pooled (1/16: no
+  // change); layernorm [32768, 768] 30.2 -> 31.8-33 us with any pool (a 30 us
+  // kernel cannot hide the claims' round trips), so it stays static.
+  static const int pool_env = [] {
+    const char* e = getenv("AFG_STREAM_POOL");
+    return e ? atoi(e) : -1;
+  }();
+  const int pool_div = pool_env >= 0 ? pool_env : (MODE == 0 ? 4 : 0);
+  unsigned int* pool_ctr = nullptr;
+  int64_t pool = 0;
+  if (pool_div > 0) {
+    pool = rows / pool_div / grp * grp;
+    static unsigned int* bases[64] = {};  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned int*& base = bases[dev & 63];
+    if (!base && cudaGetSymbolAddress(reinterpret_cast<void**>(&base), g_row_pool) != cudaSuccess)
+      base = nullptr;
+    if (base) {
+      const uintptr_t h = reinterpret_cast<uintptr_t>(s);
+      pool_ctr = base + 2 * ((h ^ (h >> 7) ^ (h >> 17)) % ROW_SLOTS);
+    } else {
+      cudaGetLastError();
+      pool = 0;
+    }
+  }
   const TI* xi = reinterpret_cast<const TI*>(x);
   const TI* ri = reinterpret_cast<const TI*>(r);
   TO* yo = reinterpret_cast<TO*>(y);
@@ -707,7 +882,7 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, xi, ri, g, b, yo, soo, rows, (int)cols, eps, ns,
-                                       slot_bytes, grp);
+                                       slot_bytes, grp, pool_ctr, pool);
     return e != cudaSuccess ? e : cudaGetLastError();
   };
   cudaError_t e;

@@ -118,3 +118,18 @@ def test_elementwise_reduce_transpose(cuda):
     assert np.array_equal(to_host(ops.transpose(x, (0, 3, 1, 2))), xh.transpose(0, 3, 1, 2))
     h = ops.convert(x, torch.float16)
     assert np.array_equal(to_host(h), O.round_to(xh, O.F16))
+
+
+@pytest.mark.parametrize("pool", ["0", "3", "16"])
+def test_stream_row_pool(cuda, pool):
+    # the streamed kernels with 1/3 or 1/16 of the rows claimed dynamically
+    # (and fully static): skip / end markers, claims, no residual, repeated
+    # launches on one stream (the pool counter resets per launch)
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, AFG_STREAM_POOL=pool)
+    out = subprocess.run([sys.executable, os.path.join(here, "stream_pool_check.py")], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
