@@ -514,6 +514,22 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
         const float bias_v = has_bias && gcol < args.N ? __ldg(args.bias + gcol) : 0.0f;
         bool bias_staged = false;
         const int acc = iter & 1;
+        if (args.residual != nullptr) {
+          // this thread's residual row segments of the tile into L2 while the
+          // tile's MMAs still run: the epilogue's loads then hit L2 instead of
+          // paying DRAM latency per chunk (BERT out-projection + residual:
+          // the synchronous loads added 19 us to a 35 us GEMM)
+          const int prow = mb * TILE_M + static_cast<int>(rank) * BLOCK_M + rloc;
+          if (prow < args.M) {
+            const char* rbase = reinterpret_cast<const char*>(args.residual) +
+                                (static_cast<int64_t>(prow) * args.ldc) * sizeof(OutT);
+            for (int cc = geff; cc < BLOCK_N / CW; cc += NG) {
+              const int n0p = nb * BLOCK_N + cc * CW;
+              if (n0p < args.N)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rbase + static_cast<int64_t>(n0p) * sizeof(OutT)));
+            }
+          }
+        }
         mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
         tc_fence_after();
         const int m0 = mb * TILE_M + static_cast<int>(rank) * BLOCK_M;
