@@ -19,6 +19,13 @@ afg_status set_error(afg_status st, const char* fmt, ...);
 afg_status cuda_status(cudaError_t e, const char* what);
 
 int num_sms();              // SM count of the current device
+// A counter slot in [0, nslots) owned by (current device, stream) for the
+// kernels that keep per-launch global counters (GEMM round sync, attention
+// unit queue, streamed-row pool): distinct streams of a device never share a
+// slot, so their concurrent launches cannot disturb each other's counters.
+// Returns -1 once a device has handed out all slots (the caller then runs the
+// counter-free variant). `kind` separates the kernels' slot spaces.
+int stream_slot(void* stream, int kind, int nslots);
 void count_launch(int n = 1);
 
 // Encodes a 2-D tiled TMA descriptor with 128-byte swizzle over a row-major

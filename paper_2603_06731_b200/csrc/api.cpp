@@ -13,7 +13,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "afg_internal.h"
 
@@ -86,6 +88,21 @@ int num_sms() {
   cached_dev = dev;
   cached_n = n > 0 ? n : 1;
   return cached_n;
+}
+
+int stream_slot(void* stream, int kind, int nslots) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, void*>, int> slots;
+  static std::map<std::pair<int, int>, int> used;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, kind, stream);
+  auto it = slots.find(key);
+  if (it != slots.end()) return it->second;
+  int& n = used[{dev, kind}];
+  if (n >= nslots) return -1;
+  return slots[key] = n++;
 }
 
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }

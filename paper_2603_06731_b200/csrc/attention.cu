@@ -70,8 +70,9 @@ struct AttnArgs {
            // 3 = MMAs back to back (no softmax dependency)
 };
 
-// Dynamic unit queue, one counter pair per slot (the host picks the slot from
-// the stream): [0] = next unit, [1] = CTA exits; the last CTA out resets both
+// Dynamic unit queue, one counter pair per slot (stream_slot: one per stream,
+// so concurrent launches on two streams never share a queue): [0] = next
+// unit, [1] = CTA exits; the last CTA out resets both
 // and the next launch on the stream touches them after griddepcontrol.wait.
 constexpr int ATTN_SLOTS = 64;
 __device__ unsigned int g_attn_queue[ATTN_SLOTS][2];
@@ -793,10 +794,8 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
     return e ? atoi(e) : 0;
   }();
   a.sched = a.sched_off = a.sched_cnt = nullptr;
-  if (a.dyn) {
-    const uintptr_t h = reinterpret_cast<uintptr_t>(s);
-    a.dyn = 1 + static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % ATTN_SLOTS);
-  } else if (sched_env) {
+  if (a.dyn) a.dyn = 1 + stream_slot(s, 1, ATTN_SLOTS);  // 0: the static walk
+  if (!a.dyn && sched_env) {
     const Sched& sc = attn_schedule(a.BH, a.Nq, a.Nk, D, a.causal, static_cast<int>(grid));
     if (sc.dev) {
       a.sched = sc.dev;

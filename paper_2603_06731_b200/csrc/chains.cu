@@ -267,11 +267,11 @@ __device__ __forceinline__ uint32_t pack_pair(uint64_t v) {
 }
 
 // Tail balancing: the last `pool` rows are not assigned to a CTA; producers
-// claim them slot by slot from a global counter (one pair per stream slot:
-// [0] = rows claimed, [1] = producer exits; the last producer out resets both,
-// the next launch touches them after griddepcontrol.wait). The per-SM DRAM
-// rates differ, so a static split ends with the slowest SM alone (layernorm:
-// SM active 45.4 k cycles on average, 48.7 k at most).
+// claim them slot by slot from a global counter pair owned by the stream
+// (stream_slot): [0] = rows claimed, [1] = producer exits; the last producer
+// out resets both, the next launch touches them after griddepcontrol.wait.
+// The per-SM DRAM rates differ, so a static split ends with the slowest SM
+// alone (layernorm: SM active 45.4 k cycles on average, 48.7 k at most).
 constexpr int ROW_SLOTS = 64;
 __device__ unsigned int g_row_pool[ROW_SLOTS][2];
 
@@ -856,9 +856,9 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
     unsigned int*& base = bases[dev & 63];
     if (!base && cudaGetSymbolAddress(reinterpret_cast<void**>(&base), g_row_pool) != cudaSuccess)
       base = nullptr;
-    if (base) {
-      const uintptr_t h = reinterpret_cast<uintptr_t>(s);
-      pool_ctr = base + 2 * ((h ^ (h >> 7) ^ (h >> 17)) % ROW_SLOTS);
+    const int slot = base ? stream_slot(s, 2, ROW_SLOTS) : -1;
+    if (slot >= 0) {
+      pool_ctr = base + 2 * slot;
     } else {
       cudaGetLastError();
       pool = 0;

@@ -58,8 +58,8 @@ struct GemmTcArgs {
                    // until every CTA has issued round r (bounded wait)
 };
 
-// Round sync counters, one pair per slot (the host picks the slot from the
-// stream, so concurrent launches on different streams do not share one):
+// Round sync counters, one pair per slot (stream_slot: one per stream, so
+// concurrent launches on different streams do not share one):
 // [0] = CTA arrivals per tile round, [1] = kernel exits. The last CTA to exit
 // resets both; the next launch on the stream touches them only after
 // griddepcontrol.wait (the previous grid has completed). A wait is bounded, so
@@ -96,8 +96,7 @@ inline int round_sync_for(int tiles, int64_t K, bool pair, cudaStream_t stream) 
     return e ? atoi(e) : 1;
   }();
   if (env <= 0 || K < 4096 || tiles < 4 * (pair ? num_sms() / 2 : num_sms())) return 0;
-  const uintptr_t h = reinterpret_cast<uintptr_t>(stream);
-  return 1 + static_cast<int>((h ^ (h >> 7) ^ (h >> 17)) % ROUND_SLOTS);
+  return 1 + stream_slot(stream, 0, ROUND_SLOTS);  // 0 (off) when the slots are used up
 }
 
 // PAIR: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile with one
@@ -964,6 +963,16 @@ bool four_epi_groups(afg_epilogue epi) {
 
 // AFG_GEMM_SHORTK_GROUPS = 2 | 4: epilogue groups of the output-bound
 // (K <= 128, BLOCK_N = 256) single-CTA GEMM
+// AFG_GEMM_SHORTK_MAXK: the largest K that takes the output-bound
+// configuration (2 stages, 4 epilogue groups)
+int64_t shortk_max_k() {
+  static const int64_t k = [] {
+    const char* e = getenv("AFG_GEMM_SHORTK_MAXK");
+    return e ? static_cast<int64_t>(atoi(e)) : 128;
+  }();
+  return k;
+}
+
 int shortk_groups() {
   static const int g = [] {
     const char* e = getenv("AFG_GEMM_SHORTK_GROUPS");
@@ -1042,7 +1051,7 @@ afg_status gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     e = dispatch_types<256, 5, true>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   // output-bound: 2 stages; 4 epilogue groups x 2 C buffers (ResNet 56x56
   // 64 -> 256 1x1: 103.6 -> 90.2 us vs 2 groups x 4 buffers)
-  else if (block_n == 256 && K <= 128 && shortk_groups() == 4)
+  else if (block_n == 256 && K <= shortk_max_k() && shortk_groups() == 4)
     e = dispatch_types<256, 2, false, 4>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);
   else if (block_n == 256 && K <= 128)  // output-bound: 2 stages, 4 C buffers per group
     e = dispatch_types<256, 2>(ab, c, b_mn_major, tmA, tmB, tmC, args, stream);

@@ -95,3 +95,28 @@ def test_simt_path_reference_shapes(cuda):
     attn_case(1, 2, 8, 4, dt=torch.float32, bias=True)
     attn_case(2, 1, 7, 16, dt=torch.float32, causal=True)
     attn_case(1, 1, 1, 4, dt=torch.float32)  # N = 1: output = V row
+
+
+def test_concurrent_streams_dynamic_queue(cuda):
+    # the dynamic unit queue keeps one counter pair per stream: two attention
+    # launches running concurrently on two streams must each produce the same
+    # result as alone (bit-identical: a unit's arithmetic does not depend on
+    # which CTA takes it)
+    outs = []
+    ins = []
+    for seed in (41, 42):
+        q, _ = seeded((4, 8, 1024, 128), "q", seed, dtype=torch.float16)
+        k, _ = seeded((4, 8, 1024, 128), "k", seed, dtype=torch.float16)
+        v, _ = seeded((4, 8, 1024, 128), "v", seed, dtype=torch.float16)
+        ins.append((q, k, v))
+        outs.append(ops.attention(q, k, v, scale=128 ** -0.5, causal=True))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(5):
+        got = []
+        for s, (q, k, v) in zip(streams, ins):
+            with torch.cuda.stream(s):
+                got.append(ops.attention(q, k, v, scale=128 ** -0.5, causal=True))
+        torch.cuda.synchronize()
+        for g, w in zip(got, outs):
+            assert torch.equal(g, w)

@@ -133,3 +133,21 @@ def test_stream_row_pool(cuda, pool):
     out = subprocess.run([sys.executable, os.path.join(here, "stream_pool_check.py")], env=env,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+
+
+def test_concurrent_streams_row_pool(cuda):
+    # the softmax tail pool keeps one counter pair per stream: concurrent
+    # launches on two streams each match their single-stream result exactly
+    g = torch.Generator(device="cuda").manual_seed(17)
+    xs = [(torch.rand((40000, 2048), generator=g, device="cuda") * 8 - 4).half() for _ in range(2)]
+    want = [ops.softmax(x) for x in xs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(5):
+        got = []
+        for s, x in zip(streams, xs):
+            with torch.cuda.stream(s):
+                got.append(ops.softmax(x))
+        torch.cuda.synchronize()
+        for a, b in zip(got, want):
+            assert torch.equal(a, b)
