@@ -43,10 +43,15 @@ using namespace sm100;
 constexpr int BM = 128;  // query rows per CTA
 constexpr int BN = 128;  // keys per KV tile
 // Bit mask over the 8 pair slots of a 16-pair group: which exponential pairs
-// use the FMA-pipe polynomial instead of MUFU ex2. Measured on B200: the
-// MUFU (16 ex2 / clk / SM) and the issue slots balance at 2 pairs in 8
-// (+4% at D = 128); 3/8 and above spill and lose 10%.
-constexpr unsigned POLY_PAIRS = 0x12;
+// use the FMA-pipe polynomial instead of MUFU ex2. Measured on B200 (round 2,
+// with the S rows loaded as register pairs, `profiles/r02/attention/
+// poly_pairs_ab.txt`): 1/8 of the pairs 1079 TFLOP/s non-causal, 903 causal;
+// 0/8 the same; 2/8 1042 / 884; 3/8 986 / 804 and 4/8 929 / 745 (spills).
+// The softmax is issue-bound, not MUFU-bound, once the pair moves are gone.
+#ifndef AFG_POLY_PAIRS
+#define AFG_POLY_PAIRS 0x02
+#endif
+constexpr unsigned POLY_PAIRS = AFG_POLY_PAIRS;
 
 
 struct AttnArgs {
