@@ -82,6 +82,17 @@ struct AttnArgs {
 constexpr int ATTN_SLOTS = 64;
 __device__ unsigned int g_attn_queue[ATTN_SLOTS][2];
 
+// Split rows (AFG_ATTN_SPLIT = 2): each query row's 128 scores are handled
+// by two threads in two warpgroups (keys [0, 64) and [64, 128) of the KV
+// tile), which exchange their partial row maxima through shared memory once
+// per step; 16 softmax warps instead of 8, half the serial work per thread.
+#ifndef AFG_ATTN_SPLIT
+#define AFG_ATTN_SPLIT 1
+#endif
+constexpr int SPLIT = AFG_ATTN_SPLIT;
+static_assert(SPLIT == 1 || SPLIT == 2, "AFG_ATTN_SPLIT");
+constexpr int ATTN_THREADS = 128 + 256 * SPLIT;
+
 template <int D>
 struct AttnSmem {
   static constexpr int TILE = BM * D * 2;  // one Q / K / V tile (BM == BN rows)
@@ -91,12 +102,17 @@ struct AttnSmem {
   // runs. Measured: +3% at D = 64 (BERT, 4-tile units); at D = 128 the two
   // K/V stages it would cost matter more (-1%), so one buffer there.
   static constexpr int QBUF = D == 64 ? 2 : 1;
-  static constexpr int STAGES = D == 64 ? (QBUF == 2 ? 8 : 10) : (QBUF == 2 ? 3 : 5);
+  // split rows need 8 KB of exchange buffers: one K/V stage fewer at D = 128
+  static constexpr int STAGES = D == 64 ? (QBUF == 2 ? 8 : 10) : (QBUF == 2 ? 3 : (SPLIT == 2 ? 4 : 5));
   static constexpr int QA_OFF = 0;
   static constexpr int QB_OFF = TILE;
   static constexpr int QBUF_BYTES = 2 * TILE;
   static constexpr int RING_OFF = QBUF * QBUF_BYTES;
-  static constexpr int BAR_OFF = RING_OFF + STAGES * TILE;
+  // row-max exchange [step parity][tile][half][row] and row-sum exchange
+  // [unit parity][tile][half][row] (floats), split rows only
+  static constexpr int XCH_OFF = RING_OFF + STAGES * TILE;
+  static constexpr int XCH_BYTES = SPLIT == 2 ? 2 * (2 * 2 * 2 * BM * 4) : 0;
+  static constexpr int BAR_OFF = XCH_OFF + XCH_BYTES;
   // q_full[QBUF], q_empty[QBUF], kv_full[S], kv_empty[S], s_full[2], p_full[2][2],
   // o_full[2], o_empty[2], unit_full[UNIT_R], unit_empty[UNIT_R]
   static constexpr int UNIT_R = 4;  // dynamic schedule: unit ids in flight (TMA -> MMA, softmax)
@@ -165,7 +181,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf16) {
 // registers to the two softmax warpgroups.
 // Warps: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4-7 softmax A, 8-11 softmax B.
 template <int D, bool BF16>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(ATTN_THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                     const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnArgs args) {
@@ -264,14 +280,16 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&p_full[2 * g], 4);  // one arrival per softmax warp of the tile
+      // one arrival per softmax warp of the tile; split rows: keys [0, 64)
+      // (and every O correction) from both halves, keys [64, 128) from half 1
+      mbar_init(&p_full[2 * g], 4 * SPLIT);
       mbar_init(&p_full[2 * g + 1], 4);
       mbar_init(&o_full[g], 1);
-      mbar_init(&o_empty[g], 4);
+      mbar_init(&o_empty[g], 4 * SPLIT);
     }
     for (int r = 0; r < L::UNIT_R; ++r) {
       mbar_init(&unit_full[r], 1);
-      mbar_init(&unit_empty[r], 9);  // the MMA warp + 8 softmax warps
+      mbar_init(&unit_empty[r], 1 + 8 * SPLIT);  // the MMA warp + the softmax warps
     }
     fence_barrier_init();
   }
@@ -286,15 +304,31 @@ __global__ void __launch_bounds__(384, 1)
   auto o_col = [](int g) { return static_cast<uint32_t>(2 * BN + g * D); };
 
   if (warp >= 4) {
-    setmaxnreg_inc<232>();
+    if constexpr (SPLIT == 2) setmaxnreg_inc<112>();
+    else setmaxnreg_inc<232>();
     // --------------------------------- softmax / correction / epilogue (per tile)
-    const int g = (warp - 4) / 4;
+    // warps 4-7: tile A, 8-11: tile B (split rows: keys [0, 64) of them; 12-15
+    // / 16-19 the same rows' keys [64, 128))
+    const int g = ((warp - 4) / 4) % 2;
+    const int h = SPLIT == 2 ? (warp - 4) / 8 : 0;
+    constexpr int SCH = NCH / SPLIT;  // 32-column S chunks per thread
+    constexpr int OCH = D / 32 / SPLIT;  // 32-column O chunks per thread
+    const int c0 = h * SCH;
+    const int oc0 = h * OCH;
     const int w4 = warp % 4;
     const int row = w4 * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
     const uint32_t s_base = lane_base + s_col(g);
     const uint32_t o_base = lane_base + o_col(g);
     uint32_t s_phase = 0;  // s_full[g] completions consumed so far (parity)
+    float* xmax = reinterpret_cast<float*>(smem + L::XCH_OFF);  // [2][2][2][BM]
+    float* xsum = xmax + 2 * 2 * 2 * BM;                          // [2][2][2][BM]
+    auto xidx = [&](int par, int hh) { return ((par * 2 + g) * 2 + hh) * BM + row; };
+    // the two warps holding the same rows of the tile (split rows only)
+    auto pair_sync = [&]() {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + 4 * g + w4) : "memory");
+    };
+    int ks = 0;  // steps taken (exchange parity)
     // this warp's TMEM writes (P half / O reads) are complete: one arrival per warp
     auto warp_arrive = [&](uint64_t* bar) {
       tc_fence_before();
@@ -313,21 +347,21 @@ __global__ void __launch_bounds__(384, 1)
                                       args.Nk
                     : nullptr;
       float m = -INFINITY;  // running max (scaled log2 units)
-      float l = 0.0f;
-      for (int j = 0; j < (args.dbg >= 3 ? 0 : nkv_g); ++j) {
+      float l = 0.0f;       // this thread's part of the row sum
+      for (int j = 0; j < (args.dbg >= 3 ? 0 : nkv_g); ++j, ++ks) {
         mbar_wait(&s_full[g], s_phase);  // also implies PV(g, j-1) completed (in-order MMAs)
         s_phase ^= 1;
         tc_fence_after();
         if (args.dbg == 1) {
           warp_arrive(&p_full[2 * g]);
-          warp_arrive(&p_full[2 * g + 1]);
+          if (SPLIT == 1 || h == 1) warp_arrive(&p_full[2 * g + 1]);
           continue;
         }
-        // the whole S row (128 fp32 scores) into registers with one TMEM pass,
-        // as 64 column pairs (the f32x2 math below takes them directly)
-        uint64_t sp[NCH][16];
+        // this thread's S columns (all 128, or one half) into registers with
+        // one TMEM pass, as column pairs (the f32x2 math takes them directly)
+        uint64_t sp[SCH][16];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) tmem_ld32x2(s_base + c * 32, sp[c]);
+        for (int c = 0; c < SCH; ++c) tmem_ld32x2(s_base + (c0 + c) * 32, sp[c]);
         tmem_wait_ld();
         auto lo = [](uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x)); };
         auto hi = [](uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x >> 32)); };
@@ -335,8 +369,8 @@ __global__ void __launch_bounds__(384, 1)
           return static_cast<uint64_t>(__float_as_uint(a)) |
                  (static_cast<uint64_t>(__float_as_uint(b)) << 32);
         };
-        const int k0 = j * BN;
-        const bool need_mask = (args.causal && k0 + BN - 1 > tile_first) || k0 + BN > args.Nk;
+        const int k0 = j * BN + c0 * 32;  // first key of this thread's columns
+        const bool need_mask = (args.causal && j * BN + BN - 1 > tile_first) || j * BN + BN > args.Nk;
         // Common path (no additive bias, scale > 0): the max is taken on the raw
         // scores, a causal-diagonal / key-tail tile masks by a per-row count of
         // valid columns (one compare + select per score), and each probability
@@ -348,7 +382,7 @@ __global__ void __launch_bounds__(384, 1)
           if (need_mask) {
             const int lim = min(args.Nk, args.causal ? qi + 1 : args.Nk) - k0;  // valid columns
 #pragma unroll
-            for (int c = 0; c < NCH; ++c)
+            for (int c = 0; c < SCH; ++c)
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const int col = c * 32 + 2 * e;
@@ -356,36 +390,44 @@ __global__ void __launch_bounds__(384, 1)
                               col + 1 >= lim ? -INFINITY : hi(sp[c][e]));
               }
           }
-          float mc[NCH];
+          float mc[SCH];
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) {
+          for (int c = 0; c < SCH; ++c) {
             mc[c] = fmax3(lo(sp[c][0]), hi(sp[c][0]), lo(sp[c][1]));
             mc[c] = fmax3(mc[c], hi(sp[c][1]), lo(sp[c][2]));
 #pragma unroll
             for (int e = 2; e < 15; ++e) mc[c] = fmax3(mc[c], hi(sp[c][e]), lo(sp[c][e + 1]));
             mc[c] = fmaxf(mc[c], hi(sp[c][15]));
           }
-          tmax = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])) * args.scale_log2;
+          float mm = mc[0];
+#pragma unroll
+          for (int c = 1; c < SCH; ++c) mm = fmaxf(mm, mc[c]);
+          tmax = mm * args.scale_log2;
           sc = args.scale_log2;
         } else {
           tmax = -INFINITY;
 #pragma unroll
-          for (int c = 0; c < NCH; ++c)
+          for (int c = 0; c < SCH; ++c)
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               float v2[2] = {lo(sp[c][e]), hi(sp[c][e])};
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int kj = k0 + c * 32 + 2 * e + h;
-                float v = v2[h] * args.scale_log2;
+              for (int hh = 0; hh < 2; ++hh) {
+                const int kj = k0 + c * 32 + 2 * e + hh;
+                float v = v2[hh] * args.scale_log2;
                 if (brow) v = kj < args.Nk ? fmaf(__ldg(brow + kj), 1.4426950408889634f, v) : v;
                 if (need_mask && (kj >= args.Nk || (args.causal && kj > qi))) v = -INFINITY;
-                v2[h] = v;
+                v2[hh] = v;
                 tmax = fmaxf(tmax, v);
               }
               sp[c][e] = pk(v2[0], v2[1]);
             }
           sc = 1.0f;
+        }
+        if constexpr (SPLIT == 2) {  // the row max over both halves
+          xmax[xidx(ks & 1, h)] = tmax;
+          pair_sync();
+          tmax = fmaxf(tmax, xmax[xidx(ks & 1, h ^ 1)]);
         }
         // lazy rescaling: the running max only moves when it grows by more than
         // 8 (log2 units; P stays <= 2^8, exact in fp16/bf16 range), so the O
@@ -396,26 +438,33 @@ __global__ void __launch_bounds__(384, 1)
         const float base = m_new == -INFINITY ? 0.0f : m_new;
         const float alpha = upd ? ex2(m - base) : 1.0f;  // 0 on the first tile
         // correction O *= exp(m_old - m_new) once per tile (warp-uniform decision:
-        // tcgen05.ld/st are warp-collective; rows whose max did not move use 1)
+        // tcgen05.ld/st are warp-collective; rows whose max did not move use 1).
+        // Split rows: each half corrects its O columns.
         if (j > 0 && __any_sync(0xffffffffu, upd)) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
+          for (int c = 0; c < OCH; ++c) {
             uint32_t o[32];
-            tmem_ld32(o_base + c * 32, o);
+            tmem_ld32(o_base + (oc0 + c) * 32, o);
             tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(o_base + c * 32, o);
+            tmem_st32(o_base + (oc0 + c) * 32, o);
           }
         }
         m = m_new;
+        // half 1's O columns are corrected: the first PV half may start once
+        // half 0's P is written too
+        if (SPLIT == 2 && h == 1) {
+          tmem_wait_st();
+          warp_arrive(&p_full[2 * g]);
+        }
         // P = exp2(sc * s - base) packed to 16 bit, written over S (P chunk c
         // lands in columns 16c..16c+15; the scores are already in registers)
         const uint64_t sc2 = pk(sc, sc), nb2 = pk(-base, -base);
-        uint64_t acc2[2] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f)};  // two chains: half the add latency
+        uint64_t acc2[2] = {pk(0.0f, 0.0f), pk(0.0f, 0.0f)};  // two chains: half the add latency
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          uint32_t pk[16];
+        for (int c = 0; c < SCH; ++c) {
+          uint32_t pkd[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const uint64_t x2 = ffma2(sp[c][e], sc2, nb2);
@@ -429,11 +478,11 @@ __global__ void __launch_bounds__(384, 1)
               p0 = ex2(x0);
               p1 = ex2(x1);
             }
-            acc2[e & 1] = fadd2(acc2[e & 1], f2(p0, p1));
-            pk[e] = pack2(p0, p1, BF16);
+            acc2[e & 1] = fadd2(acc2[e & 1], pk(p0, p1));
+            pkd[e] = pack2(p0, p1, BF16);
           }
-          tmem_st16(s_base + c * 16, pk);
-          if (c == NCH / 2 - 1) {  // keys [0, 64) of P written: the PV MMA can start
+          tmem_st16(s_base + (c0 + c) * 16, pkd);
+          if (SPLIT == 1 && c == NCH / 2 - 1) {  // keys [0, 64) of P written: the PV MMA can start
             tmem_wait_st();
             warp_arrive(&p_full[2 * g]);
           }
@@ -443,11 +492,16 @@ __global__ void __launch_bounds__(384, 1)
         f2split(acc2[1], a2, a3);
         tmem_wait_st();
         l = l * alpha + ((a0 + a1) + (a2 + a3));
-        warp_arrive(&p_full[2 * g + 1]);
+        warp_arrive(&p_full[2 * g + (SPLIT == 2 && h == 0 ? 0 : 1)]);
       }
       // ---- epilogue: O / l -> global, one 32-column chunk at a time; O_g is
       // released (o_empty) right after the last chunk's TMEM load, so the next
       // unit's first PV(g) does not wait for the global stores.
+      if constexpr (SPLIT == 2) {  // the row sum over both halves
+        xsum[xidx(u & 1, h)] = l;
+        pair_sync();
+        l += xsum[xidx(u & 1, h ^ 1)];
+      }
       mbar_wait(&o_full[g], u & 1);
       tc_fence_after();
       const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
@@ -456,13 +510,14 @@ __global__ void __launch_bounds__(384, 1)
                                static_cast<int64_t>(w.hh) * args.o_hs +
                                static_cast<int64_t>(qi) * args.o_ss;
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
+      for (int cc = 0; cc < OCH; ++cc) {
+        const int c = oc0 + cc;
         uint32_t o[32];
         if (nkv_g > 0) {
           tmem_ld32(o_base + c * 32, o);
           tmem_wait_ld();
         }
-        if (c == D / 32 - 1) warp_arrive(&o_empty[g]);
+        if (cc == OCH - 1) warp_arrive(&o_empty[g]);
         if (!valid) continue;
         if (args.o_dtype == AFG_F32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + base_idx + c * 32);
@@ -474,29 +529,30 @@ __global__ void __launch_bounds__(384, 1)
         } else {
           const bool ob = args.o_dtype == AFG_BF16;
           uint16_t* dst = reinterpret_cast<uint16_t*>(args.o) + base_idx + c * 32;
-          uint32_t w[16];
+          uint32_t wv[16];
 #pragma unroll
           for (int v = 0; v < 16; ++v)
-            w[v] = pack2(__uint_as_float(o[2 * v]) * inv_l, __uint_as_float(o[2 * v + 1]) * inv_l, ob);
+            wv[v] = pack2(__uint_as_float(o[2 * v]) * inv_l, __uint_as_float(o[2 * v + 1]) * inv_l, ob);
           if (args.o_st32) {
             // 32-byte stores: each thread writes whole sectors of its row (the
             // rows of a warp are D * 2 bytes apart, so stores do not coalesce)
 #pragma unroll
             for (int v = 0; v < 2; ++v)
               asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * v),
-                           "r"(w[8 * v]), "r"(w[8 * v + 1]), "r"(w[8 * v + 2]), "r"(w[8 * v + 3]),
-                           "r"(w[8 * v + 4]), "r"(w[8 * v + 5]), "r"(w[8 * v + 6]), "r"(w[8 * v + 7])
+                           "r"(wv[8 * v]), "r"(wv[8 * v + 1]), "r"(wv[8 * v + 2]), "r"(wv[8 * v + 3]),
+                           "r"(wv[8 * v + 4]), "r"(wv[8 * v + 5]), "r"(wv[8 * v + 6]), "r"(wv[8 * v + 7])
                            : "memory");
           } else {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) d4[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+            for (int v = 0; v < 4; ++v) d4[v] = make_uint4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
           }
         }
       }
     }
   } else {
-    setmaxnreg_dec<40>();
+    if constexpr (SPLIT == 2) setmaxnreg_dec<32>();
+    else setmaxnreg_dec<40>();
     if (warp == 0) {
       // ------------------------------------------------------------- TMA --
       if (lane == 0) {
@@ -810,7 +866,7 @@ cudaError_t launch_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(384);
+  cfg.blockDim = dim3(ATTN_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
