@@ -90,6 +90,18 @@ __device__ unsigned int g_attn_queue[ATTN_SLOTS][2];
 #define AFG_ATTN_SPLIT 1
 #endif
 constexpr int SPLIT = AFG_ATTN_SPLIT;
+// Register split between the 4 TMA / MMA / TMEM warps and the 8 softmax
+// warps: 128 x small + 256 x big must equal the CTA's launch allocation
+// (384 x 168 = 64512; a larger sum never completes setmaxnreg.inc). 40 / 232
+// spilled the MMA warp's descriptors to local memory inside the issue loop;
+// 56 / 224 removes the spills: BERT D = 64 111.7 -> 105.0 us, D = 128
+// 1109 -> 1132 TFLOP/s, causal 915 -> 937 (`profiles/r02/attention/regs_ab.txt`).
+#ifndef AFG_ATTN_REGS_SMALL
+#define AFG_ATTN_REGS_SMALL 56
+#define AFG_ATTN_REGS_BIG 224
+#endif
+static_assert(SPLIT == 2 || 128 * AFG_ATTN_REGS_SMALL + 256 * AFG_ATTN_REGS_BIG == 384 * 168,
+              "setmaxnreg split must match the launch register allocation");
 static_assert(SPLIT == 1 || SPLIT == 2, "AFG_ATTN_SPLIT");
 constexpr int ATTN_THREADS = 128 + 256 * SPLIT;
 
@@ -114,9 +126,13 @@ struct AttnSmem {
   static constexpr int XCH_BYTES = SPLIT == 2 ? 2 * (2 * 2 * 2 * BM * 4) : 0;
   static constexpr int BAR_OFF = XCH_OFF + XCH_BYTES;
   // q_full[QBUF], q_empty[QBUF], kv_full[S], kv_empty[S], s_full[2], p_full[2][2],
-  // o_full[2], o_empty[2], unit_full[UNIT_R], unit_empty[UNIT_R]
+  // o_full[OBUF][2], o_empty[OBUF][2], unit_full[UNIT_R], unit_empty[UNIT_R]
   static constexpr int UNIT_R = 4;  // dynamic schedule: unit ids in flight (TMA -> MMA, softmax)
-  static constexpr int NUM_BARS = 2 * QBUF + 2 * STAGES + 10 + 2 * UNIT_R;
+  // O accumulators per tile: two (alternating units) when they fit in TMEM
+  // next to S_A, S_B (D = 64): the next unit's PV MMAs then do not wait for
+  // this unit's epilogue to read O out of TMEM
+  static constexpr int OBUF = 2 * BN + 2 * 2 * D <= 512 ? 2 : 1;
+  static constexpr int NUM_BARS = 2 * QBUF + 2 * STAGES + 6 + 4 * OBUF + 2 * UNIT_R;
   static constexpr int TOTAL = BAR_OFF + NUM_BARS * 8 + 16 + 4 * UNIT_R + 1024;
   static_assert(TOTAL <= 232448, "attention smem over the 227 KB opt-in limit");
 };
@@ -202,9 +218,10 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   uint64_t* kv_empty = kv_full + NS;
   uint64_t* s_full = kv_empty + NS;  // [2]
   uint64_t* p_full = s_full + 2;     // [tile][half]: P columns of keys [0,64) / [64,128)
-  uint64_t* o_full = p_full + 4;     // [2]
-  uint64_t* o_empty = o_full + 2;    // [2]
-  uint64_t* unit_full = o_empty + 2;               // [UNIT_R]
+  constexpr int OBUF = L::OBUF;
+  uint64_t* o_full = p_full + 4;         // [OBUF][2]
+  uint64_t* o_empty = o_full + 2 * OBUF;  // [OBUF][2]
+  uint64_t* unit_full = o_empty + 2 * OBUF;        // [UNIT_R]
   uint64_t* unit_empty = unit_full + L::UNIT_R;    // [UNIT_R]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NUM_BARS);
   int* unit_ring = reinterpret_cast<int*>(tmem_slot + 4);  // [UNIT_R]
@@ -284,8 +301,10 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       // (and every O correction) from both halves, keys [64, 128) from half 1
       mbar_init(&p_full[2 * g], 4 * SPLIT);
       mbar_init(&p_full[2 * g + 1], 4);
-      mbar_init(&o_full[g], 1);
-      mbar_init(&o_empty[g], 4 * SPLIT);
+      for (int b = 0; b < OBUF; ++b) {
+        mbar_init(&o_full[b * 2 + g], 1);
+        mbar_init(&o_empty[b * 2 + g], 4 * SPLIT);
+      }
     }
     for (int r = 0; r < L::UNIT_R; ++r) {
       mbar_init(&unit_full[r], 1);
@@ -301,11 +320,11 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   griddep_wait();  // Q / K / V from the previous kernel are visible
   griddep_launch_dependents();
   auto s_col = [](int g) { return static_cast<uint32_t>(g * BN); };
-  auto o_col = [](int g) { return static_cast<uint32_t>(2 * BN + g * D); };
+  auto o_col = [](int g, int b) { return static_cast<uint32_t>(2 * BN + (b * 2 + g) * D); };
 
   if (warp >= 4) {
     if constexpr (SPLIT == 2) setmaxnreg_inc<112>();
-    else setmaxnreg_inc<232>();
+    else setmaxnreg_inc<AFG_ATTN_REGS_BIG>();
     // --------------------------------- softmax / correction / epilogue (per tile)
     // warps 4-7: tile A, 8-11: tile B (split rows: keys [0, 64) of them; 12-15
     // / 16-19 the same rows' keys [64, 128))
@@ -319,7 +338,6 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     const int row = w4 * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
     const uint32_t s_base = lane_base + s_col(g);
-    const uint32_t o_base = lane_base + o_col(g);
     uint32_t s_phase = 0;  // s_full[g] completions consumed so far (parity)
     float* xmax = reinterpret_cast<float*>(smem + L::XCH_OFF);  // [2][2][2][BM]
     float* xsum = xmax + 2 * 2 * 2 * BM;                          // [2][2][2][BM]
@@ -346,6 +364,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           args.bias ? args.bias + (static_cast<int64_t>(w.bh) * args.Nq + min(qi, args.Nq - 1)) *
                                       args.Nk
                     : nullptr;
+      const int ob = u % OBUF;  // this unit's O buffer
+      const uint32_t o_base = lane_base + o_col(g, ob);
       float m = -INFINITY;  // running max (scaled log2 units)
       float l = 0.0f;       // this thread's part of the row sum
       for (int j = 0; j < (args.dbg >= 3 ? 0 : nkv_g); ++j, ++ks) {
@@ -502,7 +522,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         pair_sync();
         l += xsum[xidx(u & 1, h ^ 1)];
       }
-      mbar_wait(&o_full[g], u & 1);
+      mbar_wait(&o_full[ob * 2 + g], (u / OBUF) & 1);
       tc_fence_after();
       const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
       const bool valid = qi < args.Nq && nkv_g > 0;
@@ -517,7 +537,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           tmem_ld32(o_base + c * 32, o);
           tmem_wait_ld();
         }
-        if (cc == OCH - 1) warp_arrive(&o_empty[g]);
+        if (cc == OCH - 1) warp_arrive(&o_empty[ob * 2 + g]);
         if (!valid) continue;
         if (args.o_dtype == AFG_F32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.o) + base_idx + c * 32);
@@ -552,7 +572,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
   } else {
     if constexpr (SPLIT == 2) setmaxnreg_dec<32>();
-    else setmaxnreg_dec<40>();
+    else setmaxnreg_dec<AFG_ATTN_REGS_SMALL>();
     if (warp == 0) {
       // ------------------------------------------------------------- TMA --
       if (lane == 0) {
@@ -615,6 +635,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         tc_fence_after();
       };
       int qb = 0;  // Q buffer of the current unit
+      int ob = 0;  // O buffers of the current unit
       auto issue_s = [&](int g, int j) {
         const uint64_t qd =
             q_desc0 + (g ? QB_STEP : 0) + static_cast<uint64_t>(qb) * (L::QBUF_BYTES >> 4);
@@ -636,7 +657,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 #pragma unroll
         for (int k2 = 0; k2 < BN / 32; ++k2) {
           const int kk = h * (BN / 32) + k2;
-          mma_f16_ts_if(leader, tmem + o_col(g), tmem + s_col(g) + kk * 8,
+          mma_f16_ts_if(leader, tmem + o_col(g, ob), tmem + s_col(g) + kk * 8,
                         vd + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_o,
                         (j > 0 || kk > 0) ? 1u : 0u);
         }
@@ -647,6 +668,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         const Unit w = decode(lin);
         const int nkv_max = max(w.nkv0, w.nkv1);
         qb = u % QBUF;
+        ob = u % OBUF;
         mbar_wait(&q_full[qb], (u / QBUF) & 1);
         wait_item(nb);
         if (w.nkv0 > 0) issue_s(0, 0);
@@ -661,7 +683,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           for (int g = 0; g < 2; ++g) {
             const int nkv_g = g ? w.nkv1 : w.nkv0;
             if (j < nkv_g) {
-              if (j == 0) mbar_wait(&o_empty[g], (u & 1) ^ 1);  // previous unit's O_g read
+              // the unit that last used this O buffer has read it out
+              if (j == 0) mbar_wait(&o_empty[ob * 2 + g], ((u / OBUF) & 1) ^ 1);
               // PV in two halves: the first 64 keys as soon as their P is written
               if (args.dbg < 3) mbar_wait(&p_full[2 * g], p_phase[g]);
               tc_fence_after();
@@ -677,7 +700,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
                 }
                 issue_s(g, jn);  // runs after PV(g, j) on the tensor pipe: P(j) consumed first
               } else {
-                mma_commit_if(leader, &o_full[g]);  // O_g of this unit complete
+                mma_commit_if(leader, &o_full[ob * 2 + g]);  // O_g of this unit complete
               }
             }
           }
@@ -688,8 +711,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           if ((g ? w.nkv1 : w.nkv0) == 0) {  // empty tile: keep its O phases in step
-            mbar_wait(&o_empty[g], (u & 1) ^ 1);
-            mma_commit_if(leader, &o_full[g]);
+            mbar_wait(&o_empty[ob * 2 + g], ((u / OBUF) & 1) ^ 1);
+            mma_commit_if(leader, &o_full[ob * 2 + g]);
           }
         }
         nb += 2 * nkv_max;
