@@ -297,8 +297,10 @@ class GemmSplitK:
         self.name = f"gemm_splitk_{size}"
 
     def config(self, world):
-        return {"workload": f"bf16 matmul {self.n}^3 split-K over {world} rank(s) + NCCL "
-                            f"reduce-scatter of the fp32 partials + bias/tanh-GELU epilogue",
+        how = ("NCCL reduce-scatter of the fp32 partials + bias/tanh-GELU epilogue" if world > 1
+               else "one rank: its partial is the sum, so afg_gemm_splitk runs the fused-epilogue "
+                    "GEMM (no fp32 round trip, no collective)")
+        return {"workload": f"bf16 matmul {self.n}^3 split-K over {world} rank(s), {how}",
                 "M": self.n, "N": self.n, "K": self.n, "parallelism": f"splitK/{world}",
                 "l2": "operands larger than L2"}
 

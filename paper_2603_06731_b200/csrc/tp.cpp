@@ -261,6 +261,11 @@ afg_status afg_gemm_splitk(const void* A, int64_t lda, const void* B, int64_t ld
   if (workspace_bytes < afg_gemm_splitk_workspace(M, N, world, mode) || !workspace)
     return set_error(AFG_ERR_INVALID_ARG, "afg_gemm_splitk: workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // one rank: its partial is the whole sum -- the fused-epilogue GEMM, no
+  // fp32 round trip and no collective (NCCL would only copy the buffer)
+  if (world == 1)
+    return afg_gemm(A, lda, B, ldb, bias, nullptr, C, ldc, M, N, K_local, ab_dtype, c_dtype,
+                    b_layout, epi, stream);
   // 1) this rank's fp32 partial product over its K slice (K1 on tcgen05)
   float* part = static_cast<float*>(workspace);
   st = afg_gemm(A, lda, B, ldb, nullptr, nullptr, part, N, M, N, K_local, ab_dtype, AFG_F32,
