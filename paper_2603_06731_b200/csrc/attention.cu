@@ -100,8 +100,13 @@ constexpr int SPLIT = AFG_ATTN_SPLIT;
 #define AFG_ATTN_REGS_SMALL 56
 #define AFG_ATTN_REGS_BIG 224
 #endif
-static_assert(SPLIT == 2 || 128 * AFG_ATTN_REGS_SMALL + 256 * AFG_ATTN_REGS_BIG == 384 * 168,
-              "setmaxnreg split must match the launch register allocation");
+#ifndef AFG_ATTN_REGS_SMALL64  // D = 64: the MMA warp's issue loop spills at 56
+#define AFG_ATTN_REGS_SMALL64 72   // (BERT attention 105-107 -> 103 us; 80 / 208
+#define AFG_ATTN_REGS_BIG64 216    // spills the softmax instead: 112 us)
+#endif
+static_assert(SPLIT == 2 || (128 * AFG_ATTN_REGS_SMALL + 256 * AFG_ATTN_REGS_BIG <= 384 * 168 &&
+                             128 * AFG_ATTN_REGS_SMALL64 + 256 * AFG_ATTN_REGS_BIG64 <= 384 * 168),
+              "setmaxnreg split over the launch register allocation");
 static_assert(SPLIT == 1 || SPLIT == 2, "AFG_ATTN_SPLIT");
 constexpr int ATTN_THREADS = 128 + 256 * SPLIT;
 
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 
   if (warp >= 4) {
     if constexpr (SPLIT == 2) setmaxnreg_inc<112>();
-    else setmaxnreg_inc<AFG_ATTN_REGS_BIG>();
+    else setmaxnreg_inc<D == 64 ? AFG_ATTN_REGS_BIG64 : AFG_ATTN_REGS_BIG>();
     // --------------------------------- softmax / correction / epilogue (per tile)
     // warps 4-7: tile A, 8-11: tile B (split rows: keys [0, 64) of them; 12-15
     // / 16-19 the same rows' keys [64, 128))
@@ -572,7 +577,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
   } else {
     if constexpr (SPLIT == 2) setmaxnreg_dec<32>();
-    else setmaxnreg_dec<AFG_ATTN_REGS_SMALL>();
+    else setmaxnreg_dec<D == 64 ? AFG_ATTN_REGS_SMALL64 : AFG_ATTN_REGS_SMALL>();
     if (warp == 0) {
       // ------------------------------------------------------------- TMA --
       if (lane == 0) {
