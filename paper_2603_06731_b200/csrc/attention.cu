@@ -118,7 +118,10 @@ struct AttnSmem {
   // Q buffers: with two, the next unit's Q tiles load while the current unit
   // runs. Measured: +3% at D = 64 (BERT, 4-tile units); at D = 128 the two
   // K/V stages it would cost matter more (-1%), so one buffer there.
-  static constexpr int QBUF = D == 64 ? 2 : 1;
+#ifndef AFG_ATTN_QBUF64
+#define AFG_ATTN_QBUF64 2
+#endif
+  static constexpr int QBUF = D == 64 ? AFG_ATTN_QBUF64 : 1;
   // split rows need 8 KB of exchange buffers: one K/V stage fewer at D = 128
   static constexpr int STAGES = D == 64 ? (QBUF == 2 ? 8 : 10) : (QBUF == 2 ? 3 : (SPLIT == 2 ? 4 : 5));
   static constexpr int QA_OFF = 0;
