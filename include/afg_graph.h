@@ -73,6 +73,11 @@ struct TensorValue {  // interp.h:33-44
   std::vector<int64_t> shape;
   ElementType type = ElementType::F32;
   std::vector<double> data;
+  // Optional non-owning view of numElements() doubles, read instead of `data`
+  // when set (an input the caller keeps alive for the call: the C ABI and the
+  // adapter pass their buffers without copying them). Outputs use `data`.
+  const double* view = nullptr;
+  const double* values() const { return view ? view : data.data(); }
   int64_t numElements() const {
     int64_t n = 1;
     for (int64_t d : shape) n *= d;

@@ -29,7 +29,15 @@ ElementType to_af(afg::gpu::ElementType t) {
 
 std::map<std::string, afg::gpu::TensorValue> to_afg(const std::map<std::string, TensorValue>& in) {
   std::map<std::string, afg::gpu::TensorValue> out;
-  for (const auto& [k, v] : in) out[k] = {v.shape, to_afg(v.type), v.data};
+  for (const auto& [k, v] : in) {  // views of the caller's values: no host copy
+    afg::gpu::TensorValue t;
+    t.shape = v.shape;
+    t.type = to_afg(v.type);
+    t.view = v.data.data();
+    if (static_cast<int64_t>(v.data.size()) != t.numElements()) t.data = v.data;  // let the executor report it
+    if (!t.data.empty()) t.view = nullptr;
+    out[k] = std::move(t);
+  }
   return out;
 }
 

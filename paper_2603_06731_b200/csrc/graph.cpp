@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -573,6 +574,15 @@ class Planner {
       : g_(g), opt_(o), stats_(st), R_(static_cast<cudaStream_t>(o.stream)) {}
 
   std::map<std::string, TensorValue> run(const std::map<std::string, TensorValue>& inputs) {
+    // AFG_GRAPH_TIMING=1: host-side phase times on stderr (upload / plan +
+    // launch / download), for the host-clock graph API measurements
+    static const bool timing = [] {
+      const char* e = getenv("AFG_GRAPH_TIMING");
+      return e && atoi(e) != 0;
+    }();
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     validateGraph(g_);
     if (afg_device_count() == 0)
       throw InterpError("afg: no sm_100 device visible (no CPU fallback)");
@@ -584,8 +594,11 @@ class Planner {
       const TensorDesc* d = g_.find(id);
       if (it->second.shape != d->shape) throw InterpError("input shape mismatch for %" + id);
       R_.alloc(id, d->shape, d->dtype);
-      R_.upload(id, it->second.data);
+      R_.upload(id, it->second.values(), it->second.view ? it->second.numElements()
+                                                          : static_cast<int64_t>(it->second.data.size()));
     }
+    if (timing) R_.sync("upload");
+    const auto t1 = now();
     if (opt_.fuse) find_groups();
     decide_inlining();
     for (size_t i = 0; i < g_.ops.size(); ++i) {
@@ -596,6 +609,8 @@ class Planner {
       }
       if (!inline_[i]) materialise(static_cast<int>(i));
     }
+    if (timing) R_.sync("graph execution");
+    const auto t2 = now();
     std::map<std::string, TensorValue> out;
     for (const auto& id : g_.outputIds()) {
       const TensorDesc* d = g_.find(id);
@@ -606,6 +621,9 @@ class Planner {
       out["%" + id] = std::move(v);
     }
     R_.sync("graph execution");
+    if (timing)
+      fprintf(stderr, "afg graph timing: upload %.1f ms, plan+run %.1f ms, download %.1f ms\n",
+              ms(t0, t1), ms(t1, t2), ms(t2, now()));
     return out;
   }
 
@@ -1999,12 +2017,16 @@ std::map<std::string, TensorValue> execute(const TensorGraph& g,
       auto it = inputs.find("%" + id);
       if (it == inputs.end()) it = inputs.find(id);
       if (it == inputs.end()) throw InterpError("missing input %" + id);
-      TensorValue v = it->second;
+      if (!it->second.view && static_cast<int64_t>(it->second.data.size()) != it->second.numElements())
+        throw InterpError("input shape mismatch for %" + id);
+      TensorValue v;  // a view of the caller's values: the shard's rows, or all of them
+      v.shape = it->second.shape;
+      v.type = it->second.type;
+      v.view = it->second.values();
       if (sh.count(id)) {
         const int64_t inner = v.numElements() / v.shape[0];
         v.shape[0] = rows;
-        v.data.assign(it->second.data.begin() + blocks[r].first * inner,
-                      it->second.data.begin() + blocks[r].second * inner);
+        v.view += blocks[r].first * inner;
       }
       shard_in[r]["%" + id] = std::move(v);
     }
@@ -2084,7 +2106,7 @@ AFG_API afg_status afg_graph_run(const char* graph_json, int n_inputs, const cha
       v.shape = d->shape;
       v.type = d->dtype;
       if (v.numElements() != numel[i]) throw InterpError("input shape mismatch for %" + id);
-      v.data.assign(data[i], data[i] + numel[i]);
+      v.view = data[i];  // the caller's buffer, read once on upload (no host copy)
       inputs["%" + id] = std::move(v);
     }
     GpuOptions opt;
@@ -2131,7 +2153,7 @@ AFG_API afg_status afg_graph_run_sharded(const char* graph_json, int n_inputs,
       v.shape = d->shape;
       v.type = d->dtype;
       if (v.numElements() != numel[i]) throw InterpError("input shape mismatch for %" + id);
-      v.data.assign(data[i], data[i] + numel[i]);
+      v.view = data[i];  // the caller's buffer, read once on upload (no host copy)
       inputs["%" + id] = std::move(v);
     }
     GpuOptions opt;

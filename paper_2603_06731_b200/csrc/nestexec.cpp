@@ -83,7 +83,8 @@ class ProgramRunner {
       auto it = inputs.find(b.id);
       if (it == inputs.end()) throw InterpError("missing input for buffer " + b.id);
       if (it->second.shape != b.shape) throw InterpError("input shape mismatch for buffer " + b.id);
-      R_.upload(b.id, it->second.data);
+      R_.upload(b.id, it->second.values(), it->second.view ? it->second.numElements()
+                                                            : static_cast<int64_t>(it->second.data.size()));
     }
     std::map<std::string, int> refs;
     for (const auto& top : p_.body) {

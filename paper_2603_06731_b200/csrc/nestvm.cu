@@ -28,6 +28,8 @@
 #include <stdexcept>
 #include <dlfcn.h>
 #include <mutex>
+#include <thread>
+#include <vector>
 #include <nvrtc.h>
 #include <type_traits>
 
@@ -1290,13 +1292,74 @@ void* Runner::scratch(size_t bytes) {
   return p;
 }
 
+// Large pageable host -> device copies (the graph API's inputs): the driver's
+// own pageable path stages through pinned memory with one CPU memcpy on the
+// calling thread (~10 GB/s). Here: two 64 MB pinned buffers per device, each
+// chunk copied in by four threads, then DMA'd on the stream while the next
+// chunk is copied in.
+cudaError_t staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t CH = size_t(64) << 20;
+  struct Stage {
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+  };
+  static std::mutex mu;
+  static Stage stages[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);  // one staged copy per process at a time
+  Stage& st = stages[dev & 63];
+  for (int b = 0; b < 2; ++b) {
+    if (!st.buf[b]) {
+      if (cudaHostAlloc(reinterpret_cast<void**>(&st.buf[b]), CH, cudaHostAllocDefault) != cudaSuccess ||
+          cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        st.buf[b] = nullptr;
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+      }
+    }
+  }
+  for (size_t off = 0, k = 0; off < bytes; off += CH, ++k) {
+    const int b = static_cast<int>(k & 1);
+    const size_t len = std::min(CH, bytes - off);
+    cudaError_t e = cudaEventSynchronize(st.ev[b]);  // this buffer's previous DMA is done
+    if (e != cudaSuccess) return e;
+    constexpr int T = 4;
+    const size_t per = (len / T + 63) & ~size_t(63);
+    std::thread th[T];
+    for (int t = 0; t < T; ++t) {
+      const size_t o = per * t;
+      if (o >= len) break;
+      const size_t l = std::min(per, len - o);
+      th[t] = std::thread([&, o, l] {
+        std::memcpy(st.buf[b] + o, static_cast<const char*>(src) + off + o, l);
+      });
+    }
+    for (auto& x : th)
+      if (x.joinable()) x.join();
+    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, st.buf[b], len, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaEventRecord(st.ev[b], s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaEventSynchronize(st.ev[(((bytes + CH - 1) / CH) - 1) & 1]);  // the buffers are reused
+}
+
 void Runner::upload(const std::string& id, const std::vector<double>& host) {
+  upload(id, host.data(), static_cast<int64_t>(host.size()));
+}
+
+void Runner::upload(const std::string& id, const double* host, int64_t host_n) {
   DevTensor& d = at(id);
   const int64_t n = d.numel();
-  if (static_cast<int64_t>(host.size()) != n) throw InterpError("input shape mismatch for " + id);
+  if (host_n != n) throw InterpError("input shape mismatch for " + id);
   double* tmp = static_cast<double*>(scratch(static_cast<size_t>(n) * 8));
-  cudaError_t e = cudaMemcpyAsync(tmp, host.data(), static_cast<size_t>(n) * 8,
-                                  cudaMemcpyHostToDevice, s_);
+  const size_t bytes = static_cast<size_t>(n) * 8;
+  cudaError_t e = cudaSuccess;
+  if (bytes >= (size_t(32) << 20)) {
+    e = staged_h2d(tmp, host, bytes, s_);
+  } else {
+    e = cudaMemcpyAsync(tmp, host, bytes, cudaMemcpyHostToDevice, s_);
+  }
   if (e != cudaSuccess) throw InterpError(std::string("afg: upload failed: ") + cudaGetErrorString(e));
   f64_to_native_kernel<<<grid_for(n), 256, 0, s_>>>(tmp, static_cast<char*>(d.ptr), n, d.type);
   count_launch();

@@ -67,6 +67,7 @@ class Runner {
   void release(const std::string& id);
   // Host doubles -> device, rounded to the tensor's type (interp.cpp:212-213).
   void upload(const std::string& id, const std::vector<double>& host);
+  void upload(const std::string& id, const double* host, int64_t n);
   // Device -> host doubles (exact: every stored value is representable).
   std::vector<double> download(const std::string& id);
   // Scratch device memory freed with the runner.
