@@ -1292,56 +1292,96 @@ void* Runner::scratch(size_t bytes) {
   return p;
 }
 
-// Large pageable host -> device copies (the graph API's inputs): the driver's
-// own pageable path stages through pinned memory with one CPU memcpy on the
-// calling thread (~10 GB/s). Here: two 64 MB pinned buffers per device, each
-// chunk copied in by four threads, then DMA'd on the stream while the next
-// chunk is copied in.
-cudaError_t staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  constexpr size_t CH = size_t(64) << 20;
-  struct Stage {
-    char* buf[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-  };
-  static std::mutex mu;
-  static Stage stages[64];
+// Large pageable host <-> device copies (the graph API's inputs / outputs):
+// the driver's own pageable path stages through pinned memory with one CPU
+// memcpy on the calling thread (~10 GB/s). Here: two 64 MB pinned buffers per
+// device; each chunk is copied by four threads on the host side and DMA'd on
+// the stream, the next chunk's host copy overlapping the current DMA.
+namespace {
+constexpr size_t STAGE_CH = size_t(64) << 20;
+struct Stage {
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+std::mutex g_stage_mu;  // one staged copy per process at a time
+Stage g_stage[64];
+
+Stage* stage_buffers() {
+  static const bool off = [] {  // AFG_STAGED_COPY=0: the driver's pageable copies (A/B)
+    const char* e = getenv("AFG_STAGED_COPY");
+    return e && atoi(e) == 0;
+  }();
+  if (off) return nullptr;
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);  // one staged copy per process at a time
-  Stage& st = stages[dev & 63];
+  Stage& st = g_stage[dev & 63];
   for (int b = 0; b < 2; ++b) {
     if (!st.buf[b]) {
-      if (cudaHostAlloc(reinterpret_cast<void**>(&st.buf[b]), CH, cudaHostAllocDefault) != cudaSuccess ||
+      if (cudaHostAlloc(reinterpret_cast<void**>(&st.buf[b]), STAGE_CH, cudaHostAllocDefault) !=
+              cudaSuccess ||
           cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         st.buf[b] = nullptr;
-        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+        return nullptr;
       }
     }
   }
-  for (size_t off = 0, k = 0; off < bytes; off += CH, ++k) {
+  return &st;
+}
+
+void par_memcpy(void* dst, const void* src, size_t len) {
+  constexpr int T = 4;
+  const size_t per = (len / T + 63) & ~size_t(63);
+  std::thread th[T];
+  for (int t = 0; t < T; ++t) {
+    const size_t o = per * t;
+    if (o >= len) break;
+    const size_t l = std::min(per, len - o);
+    th[t] = std::thread([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, l); });
+  }
+  for (auto& x : th)
+    if (x.joinable()) x.join();
+}
+}  // namespace
+
+cudaError_t staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Stage* st = stage_buffers();
+  if (!st) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  size_t k = 0;
+  for (size_t off = 0; off < bytes; off += STAGE_CH, ++k) {
     const int b = static_cast<int>(k & 1);
-    const size_t len = std::min(CH, bytes - off);
-    cudaError_t e = cudaEventSynchronize(st.ev[b]);  // this buffer's previous DMA is done
+    const size_t len = std::min(STAGE_CH, bytes - off);
+    cudaError_t e = cudaEventSynchronize(st->ev[b]);  // this buffer's previous DMA is done
     if (e != cudaSuccess) return e;
-    constexpr int T = 4;
-    const size_t per = (len / T + 63) & ~size_t(63);
-    std::thread th[T];
-    for (int t = 0; t < T; ++t) {
-      const size_t o = per * t;
-      if (o >= len) break;
-      const size_t l = std::min(per, len - o);
-      th[t] = std::thread([&, o, l] {
-        std::memcpy(st.buf[b] + o, static_cast<const char*>(src) + off + o, l);
-      });
-    }
-    for (auto& x : th)
-      if (x.joinable()) x.join();
-    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, st.buf[b], len, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaEventRecord(st.ev[b], s);
+    par_memcpy(st->buf[b], static_cast<const char*>(src) + off, len);
+    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, st->buf[b], len, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaEventRecord(st->ev[b], s);
     if (e != cudaSuccess) return e;
   }
-  return cudaEventSynchronize(st.ev[(((bytes + CH - 1) / CH) - 1) & 1]);  // the buffers are reused
+  return cudaEventSynchronize(st->ev[(k - 1) & 1]);  // the buffers are reused by the next call
+}
+
+cudaError_t staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Stage* st = stage_buffers();
+  if (!st) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  const size_t n = (bytes + STAGE_CH - 1) / STAGE_CH;
+  auto issue = [&](size_t k) {
+    const size_t off = k * STAGE_CH;
+    cudaError_t e = cudaMemcpyAsync(st->buf[k & 1], static_cast<const char*>(src) + off,
+                                    std::min(STAGE_CH, bytes - off), cudaMemcpyDeviceToHost, s);
+    return e == cudaSuccess ? cudaEventRecord(st->ev[k & 1], s) : e;
+  };
+  cudaError_t e = issue(0);
+  for (size_t k = 0; k < n && e == cudaSuccess; ++k) {
+    if (k + 1 < n) e = issue(k + 1);  // the next chunk's DMA overlaps this chunk's host copy
+    if (e == cudaSuccess) e = cudaEventSynchronize(st->ev[k & 1]);
+    if (e != cudaSuccess) break;
+    const size_t off = k * STAGE_CH;
+    par_memcpy(static_cast<char*>(dst) + off, st->buf[k & 1], std::min(STAGE_CH, bytes - off));
+  }
+  return e;
 }
 
 void Runner::upload(const std::string& id, const std::vector<double>& host) {
@@ -1373,8 +1413,10 @@ std::vector<double> Runner::download(const std::string& id) {
                                                     d.type);
   count_launch();
   std::vector<double> h(static_cast<size_t>(n));
-  cudaError_t e = cudaMemcpyAsync(h.data(), tmp, static_cast<size_t>(n) * 8,
-                                  cudaMemcpyDeviceToHost, s_);
+  const size_t bytes = static_cast<size_t>(n) * 8;
+  cudaError_t e = bytes >= (size_t(32) << 20)
+                      ? staged_d2h(h.data(), tmp, bytes, s_)
+                      : cudaMemcpyAsync(h.data(), tmp, bytes, cudaMemcpyDeviceToHost, s_);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s_);
   if (e != cudaSuccess) throw InterpError(std::string("afg kernel failure: ") + cudaGetErrorString(e));
   return h;

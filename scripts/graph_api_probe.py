@@ -23,7 +23,7 @@ for k in ("a", "b"):
     ins[k] = O.round_to(ins[k], O.BF16)
 print(f"inputs {time.perf_counter() - t:.2f} s", flush=True)
 text = json.dumps(g)
-for _ in range(3):
+for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     t = time.perf_counter()
     out = execute(text, ins)
     print(f"execute {1e3 * (time.perf_counter() - t):.1f} ms", flush=True)
