@@ -222,3 +222,24 @@ def test_pair_tiles_bert_ffn1_sampled(cuda):
     """BERT FFN1 at full size (B64 x S512 tokens, 768 -> 3072, erf GELU)."""
     rows = np.array([0, 1, 255, 256, 16383, 32767])
     run_case(cuda, 32768, 3072, 768, epi=Epilogue.BIAS_GELU_ERF, layout=Layout.B_NK, rows=rows)
+
+
+def test_round_sync_concurrent_streams(cuda):
+    # long-K GEMMs with many tile rounds run with the round-synchronised
+    # producers (a per-stream arrival counter): two of them concurrently on
+    # two streams must give exactly their single-stream results
+    g = torch.Generator(device="cuda").manual_seed(23)
+    a = [((torch.rand(8192, 4096, generator=g, device="cuda") - 0.5)).bfloat16() for _ in range(2)]
+    b = [((torch.rand(4096, 8192, generator=g, device="cuda") - 0.5) * 0.05).bfloat16() for _ in range(2)]
+    bias = torch.rand(8192, generator=g, device="cuda")
+    want = [ops.gemm(x, y, bias=bias, epilogue=Epilogue.BIAS_GELU_TANH) for x, y in zip(a, b)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(3):
+        got = []
+        for s, x, y in zip(streams, a, b):
+            with torch.cuda.stream(s):
+                got.append(ops.gemm(x, y, bias=bias, epilogue=Epilogue.BIAS_GELU_TANH))
+        torch.cuda.synchronize()
+        for u, v in zip(got, want):
+            assert torch.equal(u, v)
