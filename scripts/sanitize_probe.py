@@ -24,8 +24,11 @@ ops.conv2d_nhwc(x, w, torch.randn(64, device=dev), (1, 1), (1, 1), epilogue=Epil
 ops.conv2d_nhwc(x, w, torch.randn(64, device=dev), (2, 2), (1, 1), epilogue=Epilogue.BIAS_RELU)  # im2col
 q, k, v = (torch.randn(1, 2, 256, 128, device=dev).half() for _ in range(3))
 ops.attention(q, k, v, scale=128 ** -0.5, causal=True)                          # K3
+q2, k2, v2 = (torch.randn(1, 8, 1024, 64, device=dev).to(bf) for _ in range(3))
+ops.attention(q2, k2, v2, scale=64 ** -0.5)                                    # K3, D=64, unit queue
 xs = torch.randn(2048, 768, device=dev).to(bf)
 ops.layernorm_residual(xs, xs, torch.ones(768, device=dev), torch.zeros(768, device=dev))  # K5
+ops.layernorm_residual(xs, None, torch.ones(768, device=dev), torch.zeros(768, device=dev))  # no residual
 ops.softmax(torch.randn(2048, 2048, device=dev).half())                         # K4
 qa = torch.randint(-128, 128, (256, 256), dtype=torch.int8, device=dev)
 ops.gemm_i8(qa, qa, out_mode=1, scale=1 / 1024)                                 # K1c
