@@ -1080,7 +1080,13 @@ afg_status conv_tc(const void* x, const void* w, const float* bias, void* y, int
                    cudaStream_t stream) {
   const int64_t M = B * OH * OW;
   const int64_t K = KH * KW * C;
-  const int block_n = OC >= 256 ? 256 : (OC > 64 ? 128 : 64);
+  static const int conv_bn_env = [] {  // AFG_CONV_BN = 64 | 128 | 256 (A/B)
+    const char* e = getenv("AFG_CONV_BN");
+    return e ? atoi(e) : 0;
+  }();
+  const int block_n = (conv_bn_env == 64 || conv_bn_env == 128 || conv_bn_env == 256)
+                          ? conv_bn_env
+                          : (OC >= 256 ? 256 : (OC > 64 ? 128 : 64));
   const CUtensorMapDataType tdt =
       dt == AFG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   // padded bounding box: lower = -pad_begin, upper = pad_end - (K-1)*dil with
