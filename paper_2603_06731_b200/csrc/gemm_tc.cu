@@ -205,10 +205,17 @@ __device__ __forceinline__ void epi_values32(const uint32_t (&acc)[32], const Ge
     if (col0 + 32 <= a.N) {
       // bias add and activation on f32x2 pairs (one issue slot per pair)
       const float4* b4 = reinterpret_cast<const float4*>(a.bias + col0);
-      const float4* s4 = reinterpret_cast<const float4*>(sbias);
+      const uint32_t sb_addr = sbias ? smem_u32(sbias) : 0u;  // staged bias: LDS, not generic loads
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float4 b = sbias ? s4[j] : __ldg(b4 + j);
+        float4 b;
+        if (sbias) {
+          const uint4 u = ld_shared_v4(sb_addr + 16 * j);
+          b = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                          __uint_as_float(u.w));
+        } else {
+          b = __ldg(b4 + j);
+        }
         uint64_t p0 = fadd2(f2(v[4 * j], v[4 * j + 1]), f2(b.x, b.y));
         uint64_t p1 = fadd2(f2(v[4 * j + 2], v[4 * j + 3]), f2(b.z, b.w));
         p0 = apply_act2<EPI>(p0);
@@ -262,6 +269,12 @@ __device__ __forceinline__ void epi_values32_rt(const uint32_t (&acc)[32], const
 
 __device__ __forceinline__ uint32_t pack_out(float a, float b, __nv_bfloat16*) { return pack_bf16(a, b); }
 __device__ __forceinline__ uint32_t pack_out(float a, float b, __half*) { return pack_f16(a, b); }
+__device__ __forceinline__ uint32_t pack_out_relu(float a, float b, __nv_bfloat16*) {
+  return pack_bf16_relu(a, b);
+}
+__device__ __forceinline__ uint32_t pack_out_relu(float a, float b, __half*) {
+  return pack_f16_relu(a, b);
+}
 
 __device__ __forceinline__ void epi_bar_sync(int g) {
   asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
@@ -345,6 +358,13 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
   const int num_tiles = args.num_m_blocks * args.num_n_blocks;
   const int num_kb = (args.K + BLOCK_K - 1) / BLOCK_K;
 
+  // Registers: 56 for the TMA / MMA / TMEM warpgroup, the rest to the
+  // epilogue warpgroups. With setmaxnreg in the kernel ptxas allocates the
+  // launch-bound maximum (168 x 384 or 96 x 640 threads) and compiles each
+  // role's code under its own budget; the split below matches those pools
+  // (checked on every build by scripts/check_regs.py).
+  if (warp < 4) {
+  setmaxnreg_dec<56>();
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
     if (lane == 0) {
@@ -461,7 +481,9 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
       else mma_commit_if(leader, &tfull_bar[acc]);
     }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    setmaxnreg_inc<NG == 2 ? 224 : 104>();
     // ----------------------------------------------------------- epilogue --
     // NG groups of 4 warps (warps 4-7, 8-11, ...); each covers TMEM lanes
     // 0-127 (warp % 4 selects the 32-lane slice); they take column chunks
@@ -505,6 +527,9 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
       const int bcol = (geff + NG * (rloc / CW)) * CW + rloc % CW;  // tile column of my bias value
       const bool has_bias =
           args.epi != AFG_EPI_NONE && rloc < (NCHUNK - geff + NG - 1) / NG * CW && rloc < GCOLS;
+      // ReLU without a residual, 16-bit C: folded into the cvt (exact)
+      const bool relu_pack =
+          sizeof(OutT) == 2 && args.epi == AFG_EPI_BIAS_RELU && args.residual == nullptr;
       for (int t = cid; t < num_tiles; t += ncl, ++iter) {
         if (ALT && iter % NG != eg) continue;  // another group's tile
         int mb, nb;
@@ -566,8 +591,12 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
           for (int h = 0; h < CW / 32; ++h) {
             if (!live) continue;
             float v[32];
-            epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v,
-                                  sb + ((cc - geff) / NG) * CW + h * 32);
+            if (relu_pack)  // bias here, ReLU folded into the 16-bit conversion below
+              epi_values32<AFG_EPI_BIAS, OutT>(rr[h], args, row, n0 + h * 32, v,
+                                               sb + ((cc - geff) / NG) * CW + h * 32);
+            else
+              epi_values32_rt<OutT>(rr[h], args, row, n0 + h * 32, v,
+                                    sb + ((cc - geff) / NG) * CW + h * 32);
             // 32 values -> 64 B (16-bit) or 128 B (fp32) of the 128 B row
             constexpr int QPH = 32 * static_cast<int>(sizeof(OutT)) / 16;  // 16 B chunks per half
 #pragma unroll
@@ -577,7 +606,10 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
               if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                  w[k] = pack_out(v[qq * 8 + 2 * k], v[qq * 8 + 2 * k + 1], static_cast<OutT*>(nullptr));
+                  w[k] = relu_pack ? pack_out_relu(v[qq * 8 + 2 * k], v[qq * 8 + 2 * k + 1],
+                                                   static_cast<OutT*>(nullptr))
+                                   : pack_out(v[qq * 8 + 2 * k], v[qq * 8 + 2 * k + 1],
+                                              static_cast<OutT*>(nullptr));
               } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(v[qq * 4 + k]);
