@@ -282,6 +282,10 @@ struct SlotDesc {
   int n, pad;
 };
 
+#ifndef AFG_LN_ROWS  // layernorm rows per ring slot / per consumer warp step (rows <= 1024)
+#define AFG_LN_ROWS 2
+#endif
+
 template <typename TI, typename TO, int MODE, int CH>  // MODE 0 softmax, 1 layernorm
 __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     stream_rows_kernel(const TI* __restrict__ x, const TI* __restrict__ res,
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__((STREAM_WARPS + 1) * 32, 1)
     // residual + layernorm, the R rows of a slot per warp: the rows' reduction
     // chains interleave, which hides the shuffle / smem latency a single row
     // per warp leaves exposed.
-    constexpr int R = CH <= 4 ? 2 : 1;  // rows per slot (= grp at launch); long rows: 1
+    constexpr int R = CH <= 4 ? AFG_LN_ROWS : 1;  // rows per slot (= grp at launch); long rows: 1
     const uint32_t gb_addr = smem_u32(gb);
     // a lane always owns the same columns (chunks lane + 32 k): its gamma / beta
     // live in registers for the whole kernel (rows of <= 768 16-bit columns)
@@ -817,7 +821,7 @@ cudaError_t stream_launch(const void* x, const void* r, const float* g, const fl
   const int64_t nchunks = cols / E;
   // layernorm rows of <= 1024 16-bit values: two consecutive rows per ring
   // slot (one bulk copy each for x and the residual) and per consumer warp
-  const int grp = MODE == 1 && nchunks <= 128 ? 2 : 1;
+  const int grp = MODE == 1 && nchunks <= 128 ? AFG_LN_ROWS : 1;
   const int64_t row_bytes = cols * static_cast<int64_t>(sizeof(TI));
   const int slot_bytes =
       static_cast<int>(((MODE == 1 && r ? 2 : 1) * grp * row_bytes + 127) / 128 * 128);
