@@ -1266,7 +1266,14 @@ def run_afg(args, wl, rank, world, local, subs=()):
         except Exception as e:
             workloads["graph_api_gemm_gelu_4096"] = {"error": f"{type(e).__name__}: {e}"}
         release(g)
+    # each sub-workload starts after a short idle period so it does not inherit
+    # the previous measurement's power / thermal state (the chip runs under its
+    # power cap; back to back, later entries measured 5-10 % below their
+    # stand-alone --only runs)
+    cooldown = float(os.environ.get("AFG_BENCH_COOLDOWN_S", "3"))
     for name, make in subs:
+        ctx.barrier()
+        time.sleep(cooldown)
         sub = make()
         try:
             r = measure(ctx, sub, min(args.steps, 20), args.warmup, args.no_graph,
@@ -1274,6 +1281,7 @@ def run_afg(args, wl, rank, world, local, subs=()):
             workloads[name] = {k: r[k] for k in ("value", "unit", "ms_per_step", "steps",
                                                  "dtype", "roofline", "clocks", "gpu_launches")}
             workloads[name]["workload"] = r["config"].get("workload")
+            workloads[name]["cooldown_s"] = cooldown
         except Exception as e:  # report, never hide: the entry says what failed
             workloads[name] = {"error": f"{type(e).__name__}: {e}"}
         release(sub)
